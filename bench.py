@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark: windowed secure ReLU layer throughput (elements/s) on B200.
+
+Workload (BASELINE.json configs[1] at the north-star size): one ReLU layer of
+n = 2^24 fixed-point elements (x_f ~ N(0, 4^2), f = 16, N = 64), window
+(k, m) = (22, 14), i.e. the 8-bit reduced ring.  A step = both parties of one
+party pair evaluating the whole protocol (L+3 = 6 rounds) on the layer.
+
+  N = 1   one party pair time-sliced on the GPU: the fused pair kernel
+          (hb_relu_pair), openings exchanged through shared memory.
+  N > 1   (torchrun) ranks 2i / 2i+1 are parties 0 / 1 of pair i, each pair on
+          its own batch shard (weak scaling); every round is an NCCL
+          send/recv between the two ranks (staged driver, hb_relu_round).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference
+algorithm on the host instead (the oracle port, see oracle/hb_oracle.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "secure_relu_elems_per_s"
+UNIT = "elements/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--logn", type=int, default=24)
+    p.add_argument("--k", type=int, default=22)
+    p.add_argument("--m", type=int, default=14)
+    p.add_argument("--ring-bits", type=int, default=64)
+    p.add_argument("--path", choices=["pair", "staged"], default="pair", help="N=1 driver")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--sweep", default=None, help="write a (n, w) sweep table to this JSON file")
+    p.add_argument("--triple-gb", type=float, default=64.0, help="HBM budget for stocked triples")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ measured peaks / clocks
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Polls NVML (SM clock, throttle reasons) from a thread while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index=0, period=0.005):
+        self.samples, self.reasons, self.period = [], 0, period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # noqa: BLE001
+            log(f"[clocks] NVML unavailable: {exc}")
+            self.nv = None
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def algorithmic_bytes_per_elem(w: int, ring_bits: int, levels: int) -> dict:
+    """HBM bytes per element per party (DESIGN.md section 'roofline').
+
+    fused:  x (8) + y (8) + bool triples 3(1+2L)w/8 + arith triples 2*3*N/8; the
+            openings never leave the SM (shared-memory wire).
+    survey: SURVEY.md 8(d) H(w) = fused + 2 W(w) (own openings written, peer's read)."""
+    bool_b = 3 * (1 + 2 * levels) * w / 8
+    arith_b = 6 * ring_bits / 8
+    wire = (2 * w + 4 * levels * w) / 8 + 2 * 2 * ring_bits / 8
+    fused = 16 + bool_b + arith_b
+    return {"fused": fused, "survey_H": fused + 2 * wire, "wire_W": wire}
+
+
+def device_inputs(n, ring_bits, seed, device):
+    """x_f ~ N(0, 4^2) encoded at f = 16 and split (x + r, -r), generated in HBM."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    xf = torch.randn(n, generator=g, device=device, dtype=torch.float64) * 4.0
+    e = (torch.sign(xf) * torch.floor(xf.abs() * 65536.0 + 0.5)).to(torch.int64)
+    r = torch.bitwise_or(torch.bitwise_left_shift(torch.empty(n, dtype=torch.int64, device=device)
+                                                  .random_(0, 1 << 32, generator=g), 32),
+                         torch.empty(n, dtype=torch.int64, device=device).random_(0, 1 << 32, generator=g))
+    if ring_bits < 64:
+        e, r = e & ((1 << ring_bits) - 1), r & ((1 << ring_bits) - 1)
+    x0, x1 = e + r, -r
+    if ring_bits < 64:
+        x0, x1 = x0 & ((1 << ring_bits) - 1), x1 & ((1 << ring_bits) - 1)
+    return x0, x1
+
+
+def stock_sets(stores, parties, n, w, ring_bits, levels, budget_gb, want_sets, seed):
+    """Stock `sets` steps' worth of triples (fresh per step if they fit the HBM budget)."""
+    from paper_2309_04875_b200 import dealer
+
+    per_step = len(parties) * n * (3 * (1 + 2 * levels) * w / 8 + 6 * ring_bits / 8)
+    sets = int(max(1, min(want_sets, budget_gb * 1e9 // max(per_step, 1))))
+    nb, na = n * (1 + 2 * levels) * sets, 2 * n * sets
+    bt = dealer.deal_on_device(dealer.BOOL, w, nb, seed)
+    at = dealer.deal_on_device(dealer.ARITH, ring_bits, na, seed + 1)
+    for st, p in zip(stores, parties):
+        st.add_device(dealer.BOOL, w, bt[p])
+        st.add_device(dealer.ARITH, ring_bits, at[p])
+    del bt, at
+    return sets
+
+
+def check_sample(x0, x1, y0, y1, ring_bits, k, m, count=1 << 20):
+    """Reconstruction == x * drelu_from_shares on a sample (host check, not timed)."""
+    from oracle import hb_oracle as O
+
+    c = min(count, x0.numel())
+    h = [t[:c].cpu().numpy().view(np.uint64) for t in (x0, x1, y0, y1)]
+    want = O.ring_mul(O.ring_add(h[0], h[1], ring_bits), O.drelu_from_shares(h[0], h[1], ring_bits, k, m), ring_bits)
+    return bool(np.array_equal(O.ring_add(h[2], h[3], ring_bits), want))
+
+
+def cpu_baseline(k, m, ring_bits, logn_sample=20, reps=2):
+    """The reference algorithm (oracle port, two GIL-bound party threads) on the host."""
+    from oracle import hb_oracle as O
+
+    n = 1 << logn_sample
+    rng = np.random.default_rng(2024)
+    x0, x1 = O.split_additive(O.encode_fixed(rng.normal(0, 4, n), 16, ring_bits), ring_bits, rng)
+    best, eff = None, None
+    for rep in range(reps):
+        curs = O.stocked_cursors(n, k - m, ring_bits, seed=rep)
+        t0, c0 = time.perf_counter(), time.process_time()
+        O.relu_pair(x0, x1, ring_bits, k, m, curs)
+        wall, cpu = time.perf_counter() - t0, time.process_time() - c0
+        if best is None or wall < best:
+            best, eff = wall, cpu / wall
+    return {"value": n / best, "unit": UNIT, "cores": 2, "effective_cores": round(eff, 2),
+            "host_cpu_count": os.cpu_count(), "kind": "port",
+            "sample": f"{reps} runs of one ReLU layer, n=2^{logn_sample}, window ({k},{m}), best wall time; "
+                      f"oracle/hb_oracle.py (reference algorithm incl. unpackbits codec), 2 party threads"}
+
+
+# ------------------------------------------------------------------ N = 1: fused pair
+def run_single(args):
+    import torch
+
+    from paper_2309_04875_b200 import dealer, protocol, transport
+    from paper_2309_04875_b200.protocol import ProtocolSession
+    from paper_2309_04875_b200.ring import BitWindow
+    from paper_2309_04875_b200.sharing import ArithShareTensor
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n, k, m, N = 1 << args.logn, args.k, args.m, args.ring_bits
+    w = k - m
+    L = protocol.prefix_levels(w)
+    win = BitWindow(k, m)
+    eps = transport.local_pair()
+    stores = (dealer.TripleStore(0), dealer.TripleStore(1))
+    sessions = (ProtocolSession(eps[0], stores[0]), ProtocolSession(eps[1], stores[1]))
+    x0, x1 = device_inputs(n, N, 1234, dev)
+    sets = stock_sets(stores, (0, 1), n, w, N, L, args.triple_gb, args.steps + args.warmup, seed=99)
+    need = {(dealer.BOOL, w): n * (1 + 2 * L), (dealer.ARITH, N): 2 * n}
+    s = torch.cuda.current_stream()
+
+    def step(a0, a1):
+        if stores[0].remaining(dealer.BOOL, w) < need[(dealer.BOOL, w)]:
+            for st in stores:
+                st.rewind(dealer.BOOL, w)
+                st.rewind(dealer.ARITH, N)
+        if args.path == "pair":
+            return protocol.relu_pair(sessions, ArithShareTensor(0, N, a0), ArithShareTensor(1, N, a1), win)
+        return transport.run_parties(lambda: protocol.relu(sessions[0], ArithShareTensor(0, N, a0), win),
+                                     lambda: protocol.relu(sessions[1], ArithShareTensor(1, N, a1), win))
+
+    for _ in range(args.warmup):
+        y0, y1 = step(x0, x1)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(0) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t_start.record(s)
+        for i in range(args.steps):
+            ev[i][0].record(s)
+            y0, y1 = step(x0, x1)
+            ev[i][1].record(s)
+        t_end.record(s)
+        torch.cuda.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    ok = check_sample(x0, x1, y0.data, y1.data, N, k, m)
+    value = n * args.steps / (total_ms / 1e3)
+
+    bpe = algorithmic_bytes_per_elem(w, N, L)
+    peak, peak_src = peaks()
+    alg_bytes = 2 * n * bpe["fused"]
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            prof = json.load(fh)
+        key = f"pair_w{w}_n{args.logn}"
+        if key in prof:
+            traffic = prof[key]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+
+    # ---- e2e: the public API with host (pinned) buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h0 = x0.cpu().pin_memory()
+        h1 = x1.cpu().pin_memory()
+        torch.cuda.synchronize()
+        reps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            step(h0, h1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r0, r1 = step(h0, h1)
+            _ = (r0.data, r1.data)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": n * reps / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
+               "path": "protocol.relu_pair with pinned host shares in and host shares out", "steps": reps}
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline(k, m, N)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"secure ReLU layer n=2^{args.logn}, window ({k},{m}) w={w}, N={N}",
+                   "n": n, "window": [k, m], "ring_bits": N, "parties": "1 pair time-sliced on 1 GPU",
+                   "path": "fused pair kernel hb_relu_pair" if args.path == "pair" else "staged hb_relu_round x2",
+                   "inputs": "x_f~N(0,4^2), f=16, additive shares; Beaver triples from the on-device dealer",
+                   "triple_sets": sets, "l2": f"inputs {2 * n * bpe['fused'] / 1e9:.2f} GB/step > 126 MB L2",
+                   "parallelism": "pair"},
+        "correct": ok,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_elem_per_party": bpe["fused"], "survey_H_bytes_per_elem_per_party": bpe["survey_H"],
+                     "frac_vs_survey_H": (2 * n * bpe["survey_H"] / (launch_ms / 1e3) / 1e9) / peak,
+                     "kernel": f"hb::k_relu_pair<{w},128>", "launch_ms": launch_ms},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+    }
+
+
+# ------------------------------------------------------------------ N > 1: party pairs over NCCL
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_04875_b200 import dealer, protocol, transport
+    from paper_2309_04875_b200.protocol import ProtocolSession
+    from paper_2309_04875_b200.ring import BitWindow
+    from paper_2309_04875_b200.sharing import ArithShareTensor
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    pairs = world // 2
+    pair, party = rank // 2, rank % 2
+    active = pair < pairs
+    n, k, m, N = 1 << args.logn, args.k, args.m, args.ring_bits
+    w = k - m
+    L = protocol.prefix_levels(w)
+    win = BitWindow(k, m)
+    ep = transport.DistEndpoint(party, rank ^ 1) if active else None
+    store = dealer.TripleStore(party)
+    s = torch.cuda.current_stream()
+    if active:
+        # both ranks of a pair derive the same dealt values from the pair seed and keep their own share
+        x0, x1 = device_inputs(n, N, 1234 + pair, dev)
+        mine = (x0, x1)[party]
+        del x0, x1
+        sets = stock_sets((store,), (party,), n, w, N, L, args.triple_gb, args.steps + args.warmup, seed=99 + 7 * pair)
+        sess = ProtocolSession(ep, store)
+    need_b = n * (1 + 2 * L)
+
+    def step():
+        if store.remaining(dealer.BOOL, w) < need_b:
+            store.rewind(dealer.BOOL, w)
+            store.rewind(dealer.ARITH, N)
+        return protocol.relu(sess, ArithShareTensor(party, N, mine), win)
+
+    if active:
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record(s)
+        if active:
+            for _ in range(args.steps):
+                step()
+        b.record(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    out = None
+    if rank == 0:
+        value = pairs * n * args.steps / (total_ms / 1e3)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"secure ReLU layer n=2^{args.logn} per pair, window ({k},{m}) w={w}, N={N}",
+                       "n_per_pair": n, "pairs": pairs, "window": [k, m], "ring_bits": N,
+                       "path": "staged hb_relu_round + NCCL send/recv per round (ranks 2i<->2i+1)",
+                       "parallelism": f"{pairs} party pairs"},
+            "gpu_launches": args.steps * (L + 4), "clocks": clk.summary(),
+            "e2e": None,
+        }
+    dist.destroy_process_group()
+    return out
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    from oracle import hb_oracle as O
+
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return None
+    k, m, N = args.k, args.m, args.ring_bits
+    n = 1 << 18
+    rng = np.random.default_rng(2024)
+    x0, x1 = O.split_additive(O.encode_fixed(rng.normal(0, 4, n), 16, N), N, rng)
+    times, cpus = [], []
+    for i in range(args.warmup + args.steps):
+        curs = O.stocked_cursors(n, k - m, N, seed=i)
+        t0, c0 = time.perf_counter(), time.process_time()
+        O.relu_pair(x0, x1, N, k, m, curs)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+            cpus.append(time.process_time() - c0)
+    wall = sum(times)
+    value = n * len(times) / wall
+    sample = (f"per step one ReLU layer of n=2^18 (of the 2^{args.logn} workload), window ({k},{m}); "
+              f"reference algorithm via oracle/hb_oracle.py, 2 party threads")
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"secure ReLU layer n=2^{args.logn}, window ({k},{m}) w={k - m}, N={N}",
+                   "n": 1 << args.logn, "window": [k, m], "ring_bits": N, "parallelism": "host"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 2, "kind": "port", "sample": sample,
+                         "effective_cores": round(sum(cpus) / wall, 2), "host_cpu_count": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ------------------------------------------------------------------ sweep
+def run_sweep(args):
+    import copy
+
+    rows = []
+    for logn in (16, 18, 20, 22, 24, 26):
+        for k, m in ((64, 0), (32, 0), (22, 6), (22, 14), (22, 16)):
+            a = copy.copy(args)
+            a.logn, a.k, a.m = logn, k, m
+            a.no_e2e, a.no_cpu_baseline = True, True
+            a.steps = max(5, min(args.steps, 20))
+            a.warmup = 3
+            r = run_single(a)
+            row = {"logn": logn, "k": k, "m": m, "w": k - m, "elems_per_s": r["value"],
+                   "ms_per_step": r["ms_per_step"], "hbm_frac": r["roofline"]["frac"],
+                   "frac_vs_survey_H": r["roofline"]["frac_vs_survey_H"], "correct": r["correct"]}
+            log(json.dumps(row))
+            rows.append(row)
+            import torch
+
+            torch.cuda.empty_cache()
+    with open(args.sweep, "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif args.sweep:
+        run_sweep(args)
+        return
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        out = run_multi(args)
+    else:
+        out = run_single(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,131 @@
+/* hb_relu.h -- C ABI of libhbrelu.so, the B200 (sm_100a) reduced-ring secure ReLU.
+ *
+ * Drop-in boundary for the ringmpc hot path (reference: /root/reference/pkg/src/ringmpc).
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed as
+ * `void *stream` (NULL = legacy default stream); no torch types cross this boundary.
+ *
+ * Status codes mirror ringmpc/errors.py exit codes (errors.py:8-47):
+ *   HB_OK 0, HB_ERR_CUDA 1 (RingMpcError base), HB_ERR_CONFIG 2 (ConfigError/WindowError),
+ *   HB_ERR_TRANSPORT 3 (TransportError), HB_ERR_DATA 4 (DataFormatError),
+ *   HB_ERR_TRIPLES 5 (TripleExhaustedError).
+ * Every check that can fail runs on the host BEFORE any kernel or exchange, so both
+ * parties fail symmetrically (failure detection).
+ * hb_last_error() returns a thread-local message for the last failure.
+ *
+ * Data layouts (all little-endian, device memory):
+ *   arithmetic shares      uint64 residues on Z/2^N, one per element
+ *   bool triple stream     a, b, c each packed LSB-first at w bits per element into
+ *                          64-bit words (the wire layout, transport.py:33-49)
+ *   arith triple stream    a, b, c each one uint64 residue per element
+ *   payload (opening)      packed stream of 64-bit words, 8*ceil(count*w/64) bytes
+ */
+#ifndef HB_RELU_H
+#define HB_RELU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_ERR_CUDA 1
+#define HB_ERR_CONFIG 2
+#define HB_ERR_TRANSPORT 3
+#define HB_ERR_DATA 4
+#define HB_ERR_TRIPLES 5
+
+#define HB_TAG_CIRCUIT 0 /* meter tags, transport.py:26-30 */
+#define HB_TAG_MULT 1
+#define HB_TAG_B2A 2
+#define HB_TAG_OTHER 3
+
+/* One party's view of a (kind, width) triple stream, cursor-addressed like
+ * TripleStore.draw (dealer.py:152-163): the op consumes elements
+ * [cursor, cursor + need) and the caller advances its cursor afterwards. */
+typedef struct {
+  const uint64_t* a;
+  const uint64_t* b;
+  const uint64_t* c;
+  int64_t cursor;   /* first unused element */
+  int64_t capacity; /* elements in the stream */
+  int32_t width;    /* ring / word width of the stream */
+} hb_triples_t;
+
+const char* hb_last_error(void);
+int hb_version(void);
+
+/* ---- cost model (protocol.py:108-110, 202-213; transport.py:70-71) ---- */
+int hb_prefix_levels(int w);
+int64_t hb_payload_bytes(int64_t count, int w);
+/* rounds of one ReLU (drelu_only=0: L+3) or DReLU (drelu_only=1: L+2) */
+int hb_relu_rounds(int k, int m, int drelu_only);
+/* payload bytes of round r and its meter tag */
+int64_t hb_relu_round_bytes(int ring_bits, int k, int m, int64_t n, int round);
+int hb_relu_round_tag(int k, int m, int round);
+
+/* ---- 1-GPU time-sliced party pair: the whole windowed ReLU of both parties
+ * in one launch.  Replaces the two-thread run_parties(relu, relu) of
+ * protocol.py:195-199 / transport.py:271-302 when both parties share a device.
+ * y_p receives party p's output share (relu) or DReLU share (drelu_only). */
+int hb_relu_pair(int ring_bits, int k, int m, int64_t n,
+                 const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
+                 hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                 int drelu_only, void* stream);
+
+/* ---- one party, staged: protocol.relu / protocol.drelu (protocol.py:179-199)
+ * split at its exchanges.  Call round r = 0 .. hb_relu_rounds(): round r writes
+ * this party's payload of round r into `own` (hb_relu_round_bytes bytes, except
+ * the last call, which writes y) after consuming the peer's payload of round
+ * r-1 from `peer` (NULL for r = 0).  The caller exchanges own/peer between calls
+ * (Endpoint.exchange, transport.py:129-133) under tag hb_relu_round_tag(r). */
+size_t hb_relu_workspace_bytes(int k, int m, int64_t n);
+int hb_relu_round(int party, int ring_bits, int k, int m, int64_t n, int round,
+                  const uint64_t* x, uint64_t* y, hb_triples_t boolw, hb_triples_t arith,
+                  void* workspace, const uint64_t* peer, uint64_t* own, int drelu_only, void* stream);
+
+/* Same, driving the exchanges itself through a callback (the shape of
+ * protocol.relu with an Endpoint): the callback must deliver the peer's payload
+ * of `nbytes` bytes into `recv` (device memory) and return 0, or nonzero for a
+ * transport failure.  Scratch comes from `workspace` (hb_relu_callback_workspace_bytes). */
+typedef int (*hb_exchange_fn)(void* user, int tag, const uint64_t* send, uint64_t* recv, int64_t nbytes,
+                              void* stream);
+size_t hb_relu_callback_workspace_bytes(int ring_bits, int k, int m, int64_t n);
+int hb_relu(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+            hb_triples_t boolw, hb_triples_t arith, void* workspace, int drelu_only,
+            hb_exchange_fn exchange, void* user, void* stream);
+
+/* ---- wire codec (transport.py:33-67) ---- */
+int hb_pack(const uint64_t* values, int64_t count, int w, uint64_t* out, void* stream);
+int hb_unpack(const uint64_t* packed, int64_t count, int w, uint64_t* values, void* stream);
+
+/* ---- stage operations, one party (protocol.py:75-105): open = mask + pack the
+ * payload (tmp: 2*count words of scratch); close = combine with the peer's payload.
+ * kind 0 = bool (beaver_and, width-w words), kind 1 = arith (beaver_mul, Z/2^w). */
+int hb_beaver_open(int kind, int w, int64_t count, const uint64_t* x, const uint64_t* y, hb_triples_t t,
+                   uint64_t* tmp, uint64_t* payload, void* stream);
+int hb_beaver_close(int kind, int party, int w, int64_t count, const uint64_t* x, const uint64_t* y, hb_triples_t t,
+                    const uint64_t* peer_payload, uint64_t* z, void* stream);
+
+/* elementwise helpers used to compose circuit_add / a2b / b2a_bit / drelu stage by stage */
+#define HB_EW_SLICE 0     /* out = (a >> p) & mask(w)                 ring.py:69-72 */
+#define HB_EW_MSB 1       /* out = (a >> (w-1)) & 1                   ring.py:75-77 */
+#define HB_EW_XOR 2       /* out = (a ^ b) & mask(w) */
+#define HB_EW_KS_RHS 3    /* out = [(G<<2^p)&m ; (P<<2^p)&m ^ [p0]ones]  protocol.py:130-138 */
+#define HB_EW_KS_UPDATE 4 /* out = G ^ z[0:n], out2 = z[n:2n]          protocol.py:140-141 */
+#define HB_EW_KS_FINISH 5 /* out = a ^ ((b << 1) & m)                 protocol.py:142-143 */
+#define HB_EW_B2A_LIFT 6  /* out = (bit - 2 t) & m                    protocol.py:174-175 */
+#define HB_EW_DRELU_OUT 7 /* out = [p0]1 - a                          protocol.py:192 */
+#define HB_EW_OWNER 8     /* out = party == p ? a : 0                 protocol.py:153-156 */
+#define HB_EW_STACK2 9    /* out = [a ; a] */
+#define HB_EW_MASKW 10    /* out = a & mask(w) */
+int hb_ewise(int op, int party, int w, int64_t count, int p, const uint64_t* a, const uint64_t* b, uint64_t* out,
+             uint64_t* out2, void* stream);
+/* 1 if any word > 1 (b2a_bit precondition, protocol.py:166-167); synchronises `stream` */
+int hb_any_above_one(const uint64_t* a, int64_t count, int* result, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HB_RELU_H */

@@ -1,0 +1,375 @@
+// hb_api.cu -- extern "C" entry points of libhbrelu.so (declared in include/hb_relu.h).
+//
+// Host-side validation mirrors the reference's error behaviour: bad windows /
+// widths / shapes are ConfigError (ring.py:116-128, protocol.py:78-79,95-96),
+// short triple streams are TripleExhaustedError (dealer.py:152-163), and all of
+// it is decided before the first kernel or exchange so both parties fail alike.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hb_relu.h"
+#include "hb_relu_impl.cuh"
+
+using hb::u64;
+
+// ---- per-range dispatchers (hb_relu_w*.cu)
+#define HB_RANGE(lo, hi)                                                                            \
+  cudaError_t hb_pair_dispatch_##lo##_##hi(int W, const hb::PairArgs& A, cudaStream_t s);          \
+  cudaError_t hb_stage_dispatch_##lo##_##hi(int W, const hb::StageArgs& A, int L, cudaStream_t s); \
+  size_t hb_pair_smem_##lo##_##hi(int W);
+HB_RANGE(2, 8)
+HB_RANGE(9, 16)
+HB_RANGE(17, 24)
+HB_RANGE(25, 32)
+HB_RANGE(33, 40)
+HB_RANGE(41, 48)
+HB_RANGE(49, 56)
+HB_RANGE(57, 64)
+#undef HB_RANGE
+
+// ---- stage-op wrappers (hb_ops.cu)
+cudaError_t hb_ops_pack(const u64* v, u64 count, int w, u64* out, cudaStream_t s);
+cudaError_t hb_ops_unpack(const u64* in, u64 count, int w, u64* v, cudaStream_t s);
+cudaError_t hb_ops_open_mask(int kind, int w, u64 n, const u64* x, const u64* y, const u64* ta, const u64* tb, u64 cur,
+                             u64* tmp, u64* payload, cudaStream_t s);
+cudaError_t hb_ops_open_close(int kind, int party, int w, u64 n, const u64* x, const u64* y, const u64* ta,
+                              const u64* tb, const u64* tc, u64 cur, const u64* peer, u64* z, cudaStream_t s);
+cudaError_t hb_ops_ewise(int op, int party, int w, u64 n, int p, const u64* a, const u64* b, u64* out, u64* out2,
+                         cudaStream_t s);
+cudaError_t hb_ops_any_gt1(const u64* a, u64 n, int* flag_dev, cudaStream_t s);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HB_OK;
+  return fail(HB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int levels(int w) {
+  int l = 0;
+  while ((1 << l) < w) ++l;
+  return l < 1 ? 1 : l;
+}
+
+// host mirror of hb::Geo<W>
+int lane_bits(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+int group_size(int w) {
+  const int c = lane_bits(w);
+  return c <= 16 ? 8 : (c == 32 ? (w % 4 == 0 ? 2 : 8) : (w % 8 == 0 ? 1 : 8));
+}
+int group_words(int w) {
+  const int per = 64 / lane_bits(w), gs = group_size(w);
+  return (gs + per - 1) / per;
+}
+
+int64_t nbytes(int64_t count, int w) { return 8 * ((count * (int64_t)w + 63) / 64); }
+
+int check_window(int ring_bits, int k, int m) {
+  if (ring_bits < 1 || ring_bits > 64) return fail(HB_ERR_CONFIG, "ring width must be in 1..64, got %d", ring_bits);
+  if (!(0 <= m && m < k && k <= 64)) return fail(HB_ERR_CONFIG, "need 0 <= m < k <= 64, got (k=%d, m=%d)", k, m);
+  if (k - m < 2) return fail(HB_ERR_CONFIG, "window width must be >= 2, got (k=%d, m=%d)", k, m);
+  if (k > ring_bits) return fail(HB_ERR_CONFIG, "window (k=%d, m=%d) exceeds ring width %d", k, m, ring_bits);
+  return HB_OK;
+}
+
+int check_triples(const hb_triples_t& t, const char* kind, int width, int64_t need, int party) {
+  if (t.width != width)
+    return fail(HB_ERR_TRIPLES, "party %d needs %s triples of width %d, stream has width %d", party, kind, width,
+                t.width);
+  if (t.cursor < 0 || t.cursor + need > t.capacity)
+    return fail(HB_ERR_TRIPLES, "party %d needs %lld %s triples of width %d, %lld left", party, (long long)need, kind,
+                width, (long long)(t.capacity - t.cursor));
+  if (need > 0 && (!t.a || !t.b || !t.c)) return fail(HB_ERR_CONFIG, "null triple pointer");
+  return HB_OK;
+}
+
+cudaError_t pair_dispatch(int W, const hb::PairArgs& A, cudaStream_t s) {
+  if (W <= 8) return hb_pair_dispatch_2_8(W, A, s);
+  if (W <= 16) return hb_pair_dispatch_9_16(W, A, s);
+  if (W <= 24) return hb_pair_dispatch_17_24(W, A, s);
+  if (W <= 32) return hb_pair_dispatch_25_32(W, A, s);
+  if (W <= 40) return hb_pair_dispatch_33_40(W, A, s);
+  if (W <= 48) return hb_pair_dispatch_41_48(W, A, s);
+  if (W <= 56) return hb_pair_dispatch_49_56(W, A, s);
+  return hb_pair_dispatch_57_64(W, A, s);
+}
+
+cudaError_t stage_dispatch(int W, const hb::StageArgs& A, int L, cudaStream_t s) {
+  if (W <= 8) return hb_stage_dispatch_2_8(W, A, L, s);
+  if (W <= 16) return hb_stage_dispatch_9_16(W, A, L, s);
+  if (W <= 24) return hb_stage_dispatch_17_24(W, A, L, s);
+  if (W <= 32) return hb_stage_dispatch_25_32(W, A, L, s);
+  if (W <= 40) return hb_stage_dispatch_33_40(W, A, L, s);
+  if (W <= 48) return hb_stage_dispatch_41_48(W, A, L, s);
+  if (W <= 56) return hb_stage_dispatch_49_56(W, A, L, s);
+  return hb_stage_dispatch_57_64(W, A, L, s);
+}
+
+hb::PartyIO make_io(const uint64_t* x, uint64_t* y, const hb_triples_t& bw, const hb_triples_t& ar, int w) {
+  hb::PartyIO io;
+  io.x = x;
+  io.y = y;
+  io.ba = bw.a;
+  io.bb = bw.b;
+  io.bc = bw.c;
+  io.bcur = (u64)bw.cursor;
+  io.bnw = (u64)((bw.capacity * (int64_t)w + 63) / 64);
+  io.aa = ar.a;
+  io.ab = ar.b;
+  io.ac = ar.c;
+  io.acur = (u64)ar.cursor;
+  return io;
+}
+
+// workspace carve-up for the staged driver
+struct WsLayout {
+  size_t S, G, P, d, sign, total;
+};
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+WsLayout ws_layout(int w, int64_t n) {
+  const int gs = group_size(w), nw = group_words(w);
+  const size_t ng = (size_t)((n + gs - 1) / gs);
+  WsLayout L{};
+  size_t off = 0;
+  L.S = off;
+  off += align256(8 * nw * ng);
+  L.G = off;
+  off += align256(8 * nw * ng);
+  L.P = off;
+  off += align256(8 * nw * ng);
+  L.d = off;
+  off += align256(8 * (size_t)n);
+  L.sign = off;
+  off += align256(4 * ng);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hb_last_error(void) { return g_err.c_str(); }
+int hb_version(void) { return 1; }
+
+int hb_prefix_levels(int w) { return levels(w); }
+int64_t hb_payload_bytes(int64_t count, int w) { return nbytes(count, w); }
+
+int hb_relu_rounds(int k, int m, int drelu_only) { return levels(k - m) + (drelu_only ? 2 : 3); }
+
+int64_t hb_relu_round_bytes(int ring_bits, int k, int m, int64_t n, int round) {
+  const int w = k - m, L = levels(w);
+  if (round == 0) return nbytes(2 * n, w);
+  if (round <= L) return nbytes(4 * n, w);
+  return nbytes(2 * n, ring_bits);
+}
+
+int hb_relu_round_tag(int k, int m, int round) {
+  const int L = levels(k - m);
+  if (round == 0) return HB_TAG_OTHER;
+  if (round <= L) return HB_TAG_CIRCUIT;
+  if (round == L + 1) return HB_TAG_B2A;
+  return HB_TAG_MULT;
+}
+
+int hb_relu_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
+                 uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                 int drelu_only, void* stream) {
+  int rc = check_window(ring_bits, k, m);
+  if (rc) return rc;
+  if (n < 0) return fail(HB_ERR_CONFIG, "negative element count");
+  const int w = k - m, L = levels(w);
+  const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
+  if ((rc = check_triples(bool0, "bool", w, nb, 0)) || (rc = check_triples(bool1, "bool", w, nb, 1)) ||
+      (rc = check_triples(arith0, "arith", ring_bits, na, 0)) || (rc = check_triples(arith1, "arith", ring_bits, na, 1)))
+    return rc;
+  if (n == 0) return HB_OK;
+  hb::PairArgs A;
+  A.io[0] = make_io(x0, y0, bool0, arith0, w);
+  A.io[1] = make_io(x1, y1, bool1, arith1, w);
+  A.n = (u64)n;
+  A.N = ring_bits;
+  A.m = m;
+  A.drelu_only = drelu_only ? 1 : 0;
+  return cuda_status(pair_dispatch(w, A, S(stream)), "hb_relu_pair");
+}
+
+size_t hb_relu_workspace_bytes(int k, int m, int64_t n) {
+  if (k - m < 2 || k - m > 64 || n < 0) return 0;
+  return ws_layout(k - m, n).total;
+}
+
+int hb_relu_round(int party, int ring_bits, int k, int m, int64_t n, int round, const uint64_t* x, uint64_t* y,
+                  hb_triples_t boolw, hb_triples_t arith, void* workspace, const uint64_t* peer, uint64_t* own,
+                  int drelu_only, void* stream) {
+  int rc = check_window(ring_bits, k, m);
+  if (rc) return rc;
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  if (n < 0) return fail(HB_ERR_CONFIG, "negative element count");
+  const int w = k - m, L = levels(w);
+  const int last = hb_relu_rounds(k, m, drelu_only);
+  if (round < 0 || round > last) return fail(HB_ERR_CONFIG, "round %d outside 0..%d", round, last);
+  const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
+  if ((rc = check_triples(boolw, "bool", w, nb, party)) || (rc = check_triples(arith, "arith", ring_bits, na, party)))
+    return rc;
+  if (n == 0) return HB_OK;
+  if (round > 0 && !peer) return fail(HB_ERR_TRANSPORT, "round %d needs the peer payload", round);
+  const bool writes_payload = round < last;
+  if (writes_payload && !own) return fail(HB_ERR_CONFIG, "round %d needs an output payload buffer", round);
+
+  const WsLayout Lw = ws_layout(w, n);
+  char* ws = static_cast<char*>(workspace);
+  hb::StageArgs A;
+  A.io = make_io(x, y, boolw, arith, w);
+  A.n = (u64)n;
+  A.ngroups = (u64)((n + group_size(w) - 1) / group_size(w));
+  A.N = ring_bits;
+  A.m = m;
+  A.party = party;
+  A.round = round;
+  A.drelu_only = drelu_only ? 1 : 0;
+  A.bool_excl = (n % group_size(w)) == 0;
+  A.arith_excl = ring_bits == 64;
+  A.S = reinterpret_cast<u64*>(ws + Lw.S);
+  A.Gs = reinterpret_cast<u64*>(ws + Lw.G);
+  A.Ps = reinterpret_cast<u64*>(ws + Lw.P);
+  A.d = reinterpret_cast<u64*>(ws + Lw.d);
+  A.sign = reinterpret_cast<unsigned*>(ws + Lw.sign);
+  A.peer = peer;
+  const int64_t peer_segs = round == 1 ? 2 : 4;
+  A.peer_nw = (u64)((peer_segs * n * (int64_t)w + 63) / 64);
+  A.own = own;
+
+  if (writes_payload) {
+    const bool bool_round = round <= L;
+    const bool needs_zero = bool_round ? !A.bool_excl : !A.arith_excl;
+    const size_t bytes = (size_t)hb_relu_round_bytes(ring_bits, k, m, n, round);
+    if (needs_zero) {
+      cudaError_t e = cudaMemsetAsync(own, 0, bytes, S(stream));
+      if (e != cudaSuccess) return cuda_status(e, "hb_relu_round memset");
+    } else {
+      // the stream's last word is zero-padded past count*w bits (transport.py:39-49);
+      // the kernel's byte-exact stores never touch the padding, so clear that word first
+      const int64_t segs = round == 0 ? 2 : (bool_round ? 4 : 2);
+      const int64_t bits = segs * n * (int64_t)(bool_round ? w : ring_bits);
+      if (bits % 64) {
+        cudaError_t e = cudaMemsetAsync(reinterpret_cast<char*>(own) + bytes - 8, 0, 8, S(stream));
+        if (e != cudaSuccess) return cuda_status(e, "hb_relu_round pad");
+      }
+    }
+  }
+  return cuda_status(stage_dispatch(w, A, L, S(stream)), "hb_relu_round");
+}
+
+size_t hb_relu_callback_workspace_bytes(int ring_bits, int k, int m, int64_t n) {
+  if (k - m < 2 || n < 0) return 0;
+  const int w = k - m;
+  size_t pay = (size_t)nbytes(4 * n, w);
+  const size_t ar = (size_t)nbytes(2 * n, ring_bits);
+  if (ar > pay) pay = ar;
+  return hb_relu_workspace_bytes(k, m, n) + 2 * align256(pay);
+}
+
+int hb_relu(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y, hb_triples_t boolw,
+            hb_triples_t arith, void* workspace, int drelu_only, hb_exchange_fn exchange, void* user, void* stream) {
+  int rc = check_window(ring_bits, k, m);
+  if (rc) return rc;
+  if (!exchange) return fail(HB_ERR_CONFIG, "null exchange callback");
+  const int last = hb_relu_rounds(k, m, drelu_only);
+  const int w = k - m, L = levels(w);
+  const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
+  if ((rc = check_triples(boolw, "bool", w, nb, party)) || (rc = check_triples(arith, "arith", ring_bits, na, party)))
+    return rc;
+  char* ws = static_cast<char*>(workspace);
+  const size_t base = hb_relu_workspace_bytes(k, m, n);
+  size_t pay = (size_t)nbytes(4 * n, w);
+  const size_t ar = (size_t)nbytes(2 * n, ring_bits);
+  if (ar > pay) pay = ar;
+  uint64_t* own = reinterpret_cast<uint64_t*>(ws + base);
+  uint64_t* peer = reinterpret_cast<uint64_t*>(ws + base + align256(pay));
+  for (int r = 0; r <= last; ++r) {
+    rc = hb_relu_round(party, ring_bits, k, m, n, r, x, y, boolw, arith, workspace, r ? peer : nullptr,
+                       r < last ? own : nullptr, drelu_only, stream);
+    if (rc) return rc;
+    if (r < last) {
+      const int64_t bytes = hb_relu_round_bytes(ring_bits, k, m, n, r);
+      if (exchange(user, hb_relu_round_tag(k, m, r), own, peer, bytes, stream) != 0)
+        return fail(HB_ERR_TRANSPORT, "exchange failed in round %d", r);
+    }
+  }
+  return HB_OK;
+}
+
+int hb_pack(const uint64_t* values, int64_t count, int w, uint64_t* out, void* stream) {
+  if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "pack width must be in 1..64, got %d", w);
+  if (count < 0) return fail(HB_ERR_CONFIG, "negative count");
+  return cuda_status(hb_ops_pack(values, (u64)count, w, out, S(stream)), "hb_pack");
+}
+
+int hb_unpack(const uint64_t* packed, int64_t count, int w, uint64_t* values, void* stream) {
+  if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "pack width must be in 1..64, got %d", w);
+  if (count < 0) return fail(HB_ERR_CONFIG, "negative count");
+  return cuda_status(hb_ops_unpack(packed, (u64)count, w, values, S(stream)), "hb_unpack");
+}
+
+int hb_beaver_open(int kind, int w, int64_t count, const uint64_t* x, const uint64_t* y, hb_triples_t t, uint64_t* tmp,
+                   uint64_t* payload, void* stream) {
+  if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "width must be in 1..64, got %d", w);
+  if (kind != 0 && kind != 1) return fail(HB_ERR_CONFIG, "kind must be 0 (bool) or 1 (arith)");
+  int rc = check_triples(t, kind ? "arith" : "bool", w, count, -1);
+  if (rc) return rc;
+  return cuda_status(hb_ops_open_mask(kind, w, (u64)count, x, y, t.a, t.b, (u64)t.cursor, tmp, payload, S(stream)),
+                     "hb_beaver_open");
+}
+
+int hb_beaver_close(int kind, int party, int w, int64_t count, const uint64_t* x, const uint64_t* y, hb_triples_t t,
+                    const uint64_t* peer_payload, uint64_t* z, void* stream) {
+  if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "width must be in 1..64, got %d", w);
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  int rc = check_triples(t, kind ? "arith" : "bool", w, count, party);
+  if (rc) return rc;
+  return cuda_status(hb_ops_open_close(kind, party, w, (u64)count, x, y, t.a, t.b, t.c, (u64)t.cursor, peer_payload, z,
+                                       S(stream)),
+                     "hb_beaver_close");
+}
+
+int hb_ewise(int op, int party, int w, int64_t count, int p, const uint64_t* a, const uint64_t* b, uint64_t* out,
+             uint64_t* out2, void* stream) {
+  if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "width must be in 1..64, got %d", w);
+  if (op < HB_EW_SLICE || op > HB_EW_MASKW) return fail(HB_ERR_CONFIG, "unknown elementwise op %d", op);
+  return cuda_status(hb_ops_ewise(op, party, w, (u64)count, p, a, b, out, out2, S(stream)), "hb_ewise");
+}
+
+int hb_any_above_one(const uint64_t* a, int64_t count, int* result, void* stream) {
+  int* flag = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "hb_any_above_one alloc");
+  e = hb_ops_any_gt1(a, (u64)count, flag, S(stream));
+  int host = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&host, flag, sizeof(int), cudaMemcpyDeviceToHost, S(stream));
+  cudaFreeAsync(flag, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "hb_any_above_one");
+  *result = host;
+  return HB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+"""CPU-only checks: the C ABI loads and exports every declared symbol, the
+host-side cost model / metering / configuration / dealer logic, and the
+endpoints (LocalEndpoint, TCP, torch.distributed gloo with world_size 2)."""
+
+import hashlib
+import os
+import re
+import socket
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import hb_oracle as O
+from paper_2309_04875_b200 import _lib, dealer, protocol, transport
+from paper_2309_04875_b200.errors import (ConfigError, DataFormatError, TransportError, TripleExhaustedError,
+                                          WindowError)
+from paper_2309_04875_b200.ring import BitWindow, FixedPointConfig
+from paper_2309_04875_b200.transport import Meter, local_pair, run_parties
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_abi_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "hb_relu.h")).read()
+    declared = set(re.findall(r"\b(hb_\w+)\s*\(", header))
+    lib = _lib.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTED)
+
+
+@pytest.mark.parametrize("w", [2, 3, 4, 6, 8, 13, 16, 21, 32, 64])
+def test_cost_model_matches_oracle(w):
+    lib = _lib.load()
+    assert lib.hb_prefix_levels(w) == protocol.prefix_levels(w) == O.levels_for(w)
+    for n in (1, 37, 1000, 1 << 20):
+        k, m = (w, 0)
+        trace = protocol.relu_trace(n, BitWindow(k, m), 64)
+        assert trace == O.analytic_trace(n, w, 64)
+        assert trace[:-1] == protocol.relu_trace(n, BitWindow(k, m), 64, drelu_only=True)
+        assert lib.hb_payload_bytes(n, w) == O.stream_nbytes(n, w)
+
+
+def test_abi_rejects_bad_configs_before_any_kernel():
+    lib = _lib.load()
+    t = _lib.Triples(0, 0, 0, 0, 0, 8)
+    for ring_bits, k, m in ((64, 5, 4), (64, 65, 0), (16, 20, 4), (0, 8, 0)):
+        rc = lib.hb_relu_pair(ring_bits, k, m, 8, None, None, None, None, t, t, t, t, 0, None)
+        assert rc == _lib.HB_ERR_CONFIG
+    rc = lib.hb_relu_pair(64, 8, 0, 8, None, None, None, None, t, t, _lib.Triples(0, 0, 0, 0, 0, 64),
+                          _lib.Triples(0, 0, 0, 0, 0, 64), 0, None)
+    assert rc == _lib.HB_ERR_TRIPLES
+    with pytest.raises(TripleExhaustedError):
+        _lib.check(rc)
+    assert b"needs" in lib.hb_last_error()
+
+
+def test_window_validation():
+    for k, m in ((5, 4), (65, 0), (3, 3), (2, -1)):
+        with pytest.raises(WindowError):
+            BitWindow(k, m)
+    with pytest.raises(WindowError):
+        BitWindow(20, 4).check_fits(16)
+    assert BitWindow(22, 14).width == 8
+    assert BitWindow.from_json(BitWindow(9, 2).to_json()) == BitWindow(9, 2)
+    with pytest.raises(ConfigError):
+        FixedPointConfig(64, 0)
+
+
+def test_meter_semantics():
+    m = Meter()
+    m.record(10)
+    assert m.bytes_sent["Other"] == 10 and m.rounds["Other"] == 1
+    m = Meter()
+    with m.tag("Circuit"):
+        m.record(1)
+        with m.tag("B2A"):
+            m.record(2)
+        m.record(4)
+    m.record(8)
+    assert m.bytes_sent == {"Circuit": 5, "Mult": 0, "B2A": 2, "Other": 8}
+    assert m.trace == [("Circuit", 1), ("B2A", 2), ("Circuit", 4), ("Other", 8)]
+    with pytest.raises(ConfigError):
+        with m.tag("Bogus"):
+            pass
+
+
+def test_dealer_golden_sha(tmp_path, golden):
+    meta, _ = golden
+    p = tmp_path / "g.bin"
+    dealer.save_triples(dealer.gen_arith_triples(1000, 16, seed=1234), p)
+    assert hashlib.sha256(p.read_bytes()).hexdigest() == meta["dealer_hbtrip1_sha"]["sha"]
+    assert hashlib.sha256(p.read_bytes()).hexdigest() == "4df0822d744dc28807cbc8b47e94711a0baac20e57a38722342f76599396ac3f"
+    for key, want in meta["dealer_streams"].items():
+        kind, w, seed, cnt = key.split("_")
+        gen = dealer.gen_arith_triples if kind == "arith" else dealer.gen_bool_triples
+        b = gen(int(cnt), int(w), int(seed))
+        assert [O.digest(a) for p_ in (0, 1) for a in b.party_arrays(p_)] == want
+
+
+def test_triple_file_roundtrip_and_errors(tmp_path):
+    for batch in (dealer.gen_arith_triples(257, 24, seed=9), dealer.gen_bool_triples(31, 5, seed=10)):
+        path = tmp_path / f"{batch.kind}.bin"
+        dealer.save_triples(batch, path)
+        got = dealer.load_triples(path)
+        assert (got.kind, got.width, got.count, got.seed) == (batch.kind, batch.width, batch.count, batch.seed)
+        for p in (0, 1):
+            for x, y in zip(got.party_arrays(p), batch.party_arrays(p)):
+                assert np.array_equal(x, y)
+    blob = (tmp_path / "arith.bin").read_bytes()
+    for bad in (blob[:-8], b"NOTMAGIC" + blob[8:], blob[:10]):
+        (tmp_path / "bad.bin").write_bytes(bad)
+        with pytest.raises(DataFormatError):
+            dealer.load_triples(tmp_path / "bad.bin")
+
+
+def test_local_pair_bytes_and_close():
+    ep0, ep1 = local_pair()
+    r0, r1 = run_parties(lambda: ep0.exchange(b"from0"), lambda: ep1.exchange(b"from1"))
+    assert r0 == b"from1" and r1 == b"from0"
+    assert ep0.meter.total_bytes() == 5 and ep0.meter.total_rounds() == 1
+    ep0, ep1 = local_pair()
+    ep1.close()
+    with pytest.raises(TransportError):
+        ep0.exchange(b"hello")
+    ep0, ep1 = local_pair()
+
+    def bad():
+        raise ValueError("boom")
+
+    with pytest.raises(ValueError, match="boom"):
+        run_parties(bad, lambda: ep1.exchange(b"x"), endpoints=(ep0, ep1))
+
+
+def test_length_mismatch_is_transport_error():
+    ep0, ep1 = local_pair()
+    with pytest.raises(TransportError):
+        run_parties(lambda: ep0.exchange(b"abcd"), lambda: ep1.exchange(b"ab"), endpoints=(ep0, ep1))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_tcp_loopback_exchange():
+    port = _free_port()
+    out = {}
+
+    def serve():
+        ep = transport.tcp_listen("127.0.0.1", port)
+        out[0] = ep.exchange(b"a" * 100_000)
+        ep.close()
+
+    def dial():
+        ep = transport.tcp_connect("127.0.0.1", port)
+        out[1] = ep.exchange(b"b" * 100_000)
+        ep.close()
+
+    ts = [threading.Thread(target=serve), threading.Thread(target=dial)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(30)
+    assert out[0] == b"b" * 100_000 and out[1] == b"a" * 100_000
+
+
+def _dist_worker(rank, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    ep = transport.DistEndpoint(rank % 2, rank ^ 1)
+    got = []
+    with ep.tag("Circuit"):
+        for i in range(3):
+            got.append(ep.exchange(bytes([rank]) * (8 * (i + 1))))
+    q.put((rank, got, ep.meter.to_json()))
+    dist.destroy_process_group()
+
+
+def test_dist_endpoint_gloo_world2():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_dist_worker, args=(r, port, q)) for r in (0, 1)]
+    for p in ps:
+        p.start()
+    res = dict((r, (g, m)) for r, g, m in (q.get(timeout=120) for _ in ps))
+    for p in ps:
+        p.join(60)
+    assert res[0][0] == [bytes([1]) * 8, bytes([1]) * 16, bytes([1]) * 24]
+    assert res[1][0] == [bytes([0]) * 8, bytes([0]) * 16, bytes([0]) * 24]
+    assert res[0][1]["tags"]["Circuit"] == {"bytes": 48, "rounds": 3}
