@@ -160,12 +160,8 @@ def stock_sets(stores, parties, n, w, ring_bits, levels, budget_gb, want_sets, s
     per_step = len(parties) * n * (3 * (1 + 2 * levels) * w / 8 + 6 * ring_bits / 8)
     sets = int(max(1, min(want_sets, budget_gb * 1e9 // max(per_step, 1))))
     nb, na = n * (1 + 2 * levels) * sets, 2 * n * sets
-    bt = dealer.deal_on_device(dealer.BOOL, w, nb, seed)
-    at = dealer.deal_on_device(dealer.ARITH, ring_bits, na, seed + 1)
-    for st, p in zip(stores, parties):
-        st.add_device(dealer.BOOL, w, bt[p])
-        st.add_device(dealer.ARITH, ring_bits, at[p])
-    del bt, at
+    dealer.stock_on_device(stores, parties, dealer.BOOL, w, nb, seed)
+    dealer.stock_on_device(stores, parties, dealer.ARITH, ring_bits, na, seed + 1)
     return sets
 
 

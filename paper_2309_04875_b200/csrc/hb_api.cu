@@ -67,16 +67,8 @@ int levels(int w) {
   return l < 1 ? 1 : l;
 }
 
-// host mirror of hb::Geo<W>
-int lane_bits(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
-int group_size(int w) {
-  const int c = lane_bits(w);
-  return c <= 16 ? 8 : (c == 32 ? (w % 4 == 0 ? 2 : 8) : (w % 8 == 0 ? 1 : 8));
-}
-int group_words(int w) {
-  const int per = 64 / lane_bits(w), gs = group_size(w);
-  return (gs + per - 1) / per;
-}
+int group_size(int w) { return hb::group_size_for(w); }
+int group_words(int w) { return hb::group_words_for(w); }
 
 int64_t nbytes(int64_t count, int w) { return 8 * ((count * (int64_t)w + 63) / 64); }
 

@@ -33,11 +33,28 @@ HB_DEV void atom_or(u64* p, u64 v) {
   atomicOr(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
+// Lane bits and elements per group as functions of the width, shared by the
+// kernels (Geo<W>) and the host-side launch / workspace arithmetic.
+//   lane bits C: next power of two >= w, at least 8.
+//   group size : the fewest elements whose packed bits are whole bytes, raised so
+//                a group spans at least 32 packed bits for narrow lanes.  Small
+//                groups keep every load of a tile in registers at once (more bytes
+//                in flight per SM).
+__host__ __device__ constexpr int lane_bits_for(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+__host__ __device__ constexpr int group_size_for(int w) {
+  const int by = w % 8 == 0 ? 1 : (w % 4 == 0 ? 2 : (w % 2 == 0 ? 4 : 8));
+  const int c = lane_bits_for(w);
+  return c == 64 ? by : (c == 32 ? (by < 2 ? 2 : by) : (by < 4 ? 4 : by));
+}
+__host__ __device__ constexpr int group_words_for(int w) {
+  return (group_size_for(w) + (64 / lane_bits_for(w)) - 1) / (64 / lane_bits_for(w));
+}
+
 template <int W>
 struct Geo {
   static_assert(W >= 1 && W <= 64, "width must be in 1..64");
-  static constexpr int C = W <= 8 ? 8 : W <= 16 ? 16 : W <= 32 ? 32 : 64;   // lane bits
-  static constexpr int GS = C <= 16 ? 8 : (C == 32 ? (W % 4 == 0 ? 2 : 8) : (W % 8 == 0 ? 1 : 8));
+  static constexpr int C = lane_bits_for(W);
+  static constexpr int GS = group_size_for(W);
   static constexpr int PER = 64 / C;                    // lanes per word
   static constexpr int NW = (GS + PER - 1) / PER;       // container words per group
   static constexpr int PB = GS * W;                     // packed bits per group (multiple of 8)
@@ -168,28 +185,71 @@ HB_DEV u64 ldg64(const u64* p) { return (u64)__ldg(reinterpret_cast<const unsign
 
 // Read the packed bits of the group whose first element is stream element `e`
 // (any bit alignment).  Words at or beyond `nwords` read as zero.
+HB_DEV uint32_t ldg32(const uint32_t* p) { return __ldg(p); }
+
+// Read the packed bits of the group whose first element is stream element `e`
+// (any bit alignment).  Words at or beyond `nwords` read as zero.  Groups of at
+// most 32 bits use 32-bit loads (one load when the group does not straddle).
 template <int W>
 HB_DEV Pk<W> load_pk(const u64* __restrict__ s, u64 e, u64 nwords) {
   using G = Geo<W>;
   const u64 B = e * (u64)W;
-  const u64 w0 = B >> 6;
-  const int sh = (int)(B & 63);
   Pk<W> p;
-  if (sh == 0) {
-#pragma unroll
-    for (int k = 0; k < G::PW; ++k) p.v[k] = (w0 + k < nwords) ? ldg64(s + w0 + k) : 0ull;
+  if constexpr (G::PB <= 32) {
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(s);
+    const u64 n32 = 2 * nwords, w0 = B >> 5;
+    const int sh = (int)(B & 31);
+    u64 v = (w0 < n32) ? (u64)ldg32(s32 + w0) : 0ull;
+    if (sh + G::PB > 32 && w0 + 1 < n32) v |= (u64)ldg32(s32 + w0 + 1) << 32;
+    p.v[0] = (v >> sh) & ((1ull << G::PB) - 1);
+    return p;
   } else {
-    u64 prev = (w0 < nwords) ? ldg64(s + w0) : 0ull;
+    const u64 w0 = B >> 6;
+    const int sh = (int)(B & 63);
+    if (sh == 0) {
 #pragma unroll
-    for (int k = 0; k < G::PW; ++k) {
-      const bool need = (sh + G::PB - 64 * k) > 64;  // bits continue into the next word
-      const u64 nxt = (need && w0 + k + 1 < nwords) ? ldg64(s + w0 + k + 1) : 0ull;
-      p.v[k] = (prev >> sh) | (nxt << (64 - sh));
-      prev = nxt;
+      for (int k = 0; k < G::PW; ++k) p.v[k] = (w0 + k < nwords) ? ldg64(s + w0 + k) : 0ull;
+    } else {
+      u64 prev = (w0 < nwords) ? ldg64(s + w0) : 0ull;
+#pragma unroll
+      for (int k = 0; k < G::PW; ++k) {
+        const bool need = (sh + G::PB - 64 * k) > 64;  // bits continue into the next word
+        const u64 nxt = (need && w0 + k + 1 < nwords) ? ldg64(s + w0 + k + 1) : 0ull;
+        p.v[k] = (prev >> sh) | (nxt << (64 - sh));
+        prev = nxt;
+      }
     }
+    if constexpr (G::PB % 64 != 0) p.v[G::PW - 1] &= (1ull << (G::PB % 64)) - 1;
+    return p;
   }
-  if constexpr (G::PB % 64 != 0) p.v[G::PW - 1] &= (1ull << (G::PB % 64)) - 1;
-  return p;
+}
+
+// GS consecutive uint64 elements starting at p (128-bit loads when aligned).
+template <int GS>
+HB_DEV void load_u64s(const u64* __restrict__ p, int valid, u64 (&out)[GS]) {
+  if (valid == GS && GS % 2 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int j = 0; j < GS; j += 2) {
+      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p + j));
+      out[j] = v.x;
+      out[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < GS; ++j) out[j] = (j < valid) ? ldg64(p + j) : 0ull;
+  }
+}
+
+template <int GS>
+HB_DEV void store_u64s(u64* __restrict__ p, int valid, const u64 (&v)[GS]) {
+  if (valid == GS && GS % 2 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int j = 0; j < GS; j += 2) *reinterpret_cast<ulonglong2*>(p + j) = make_ulonglong2(v[j], v[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < GS; ++j)
+      if (j < valid) p[j] = v[j];
+  }
 }
 
 template <int W>

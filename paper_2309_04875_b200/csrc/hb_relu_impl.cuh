@@ -125,7 +125,7 @@ template <int W, int TP>
 __global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
   using G = Geo<W>;
   using K = Kit<W>;
-  constexpr int GS = G::GS, PW = G::PW, SEGW = PairGeo<W>::SEGW;
+  constexpr int GS = G::GS, PW = G::PW, SEGW = PairGeo<W>::SEGW, L = K::L, NSEG = 1 + 2 * L;
   extern __shared__ u64 wire[];  // [buf 2][party 2][SEGW][TP]
 
   const int party = threadIdx.x >= TP ? 1 : 0;
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
   const int valid = e0 >= n ? 0 : (int)min((u64)GS, n - e0);
   const PartyIO& io = A.io[party];
   const u64 MN = nmask(A.N);
+  const bool mult = !A.drelu_only;
 
   auto slot = [&](int buf, int who, int k) -> u64& { return wire[((buf * 2 + who) * SEGW + k) * TP + t]; };
   auto put_pk = [&](int buf, int k0, const Cg<W>& v) {
@@ -150,92 +151,95 @@ __global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
     return from_packed<W>(p);
   };
 
-  // ---- slice (local)
+  // ---- every load of this tile is issued up front (memory-level parallelism):
+  //      the share, all 1+2L bool triple segments, both arith triple segments.
+  //      Bool segment s: 0 = Other, 1+2l = level l g-part, 2+2l = level l p-part.
   u64 x[GS];
+  load_u64s<GS>(io.x + e0, valid, x);
+  Cg<W> ta[NSEG], tbv[NSEG], tc[NSEG];
 #pragma unroll
-  for (int j = 0; j < GS; ++j) x[j] = (j < valid) ? io.x[e0 + j] : 0ull;
+  for (int sgi = 0; sgi < NSEG; ++sgi) {
+    const u64 e = io.bcur + (u64)sgi * n + e0;
+    ta[sgi] = load_cg<W>(io.ba, e, io.bnw);
+    tbv[sgi] = load_cg<W>(io.bb, e, io.bnw);
+    tc[sgi] = load_cg<W>(io.bc, e, io.bnw);
+  }
+  u64 a1[GS], b1[GS], c1[GS], a2[GS], b2[GS], c2[GS];
+  const u64 ta0 = io.acur + e0;
+  load_u64s<GS>(io.aa + ta0, valid, a1);
+  load_u64s<GS>(io.ab + ta0, valid, b1);
+  load_u64s<GS>(io.ac + ta0, valid, c1);
+  if (mult) {
+    load_u64s<GS>(io.aa + ta0 + n, valid, a2);
+    load_u64s<GS>(io.ab + ta0 + n, valid, b2);
+    load_u64s<GS>(io.ac + ta0 + n, valid, c2);
+  }
+
+  // ---- slice (local)
   const Cg<W> S = K::slice(x, A.m);
 
   // ---- round 0: generate bits G = AND(u, v)
-  const u64 tb = io.bcur;
   Cg<W> Gc, P = S;
   {
-    const Cg<W> a = load_cg<W>(io.ba, tb + e0, io.bnw);
-    const Cg<W> b = load_cg<W>(io.bb, tb + e0, io.bnw);
-    const Cg<W> c = load_cg<W>(io.bc, tb + e0, io.bnw);
     const Cg<W> z0 = cg_zero<W>();
-    const Cg<W> e = (p0 ? S : z0) ^ a;
-    const Cg<W> f = (p0 ? z0 : S) ^ b;
+    const Cg<W> e = (p0 ? S : z0) ^ ta[0];
+    const Cg<W> f = (p0 ? z0 : S) ^ tbv[0];
     put_pk(0, 0, e);
     put_pk(0, PW, f);
     __syncthreads();
-    Gc = K::and_z(p0, e ^ get_pk(0, 0), f ^ get_pk(0, PW), a, b, c);
+    Gc = K::and_z(p0, e ^ get_pk(0, 0), f ^ get_pk(0, PW), ta[0], tbv[0], tc[0]);
   }
 
   // ---- rounds 1..L: Kogge-Stone levels
-#pragma unroll 1
-  for (int l = 0; l < K::L; ++l) {
-    const int buf = (l + 1) & 1;
-    const u64 base = tb + n + 2 * n * (u64)l + e0;
-    const Cg<W> ag = load_cg<W>(io.ba, base, io.bnw), bg = load_cg<W>(io.bb, base, io.bnw);
-    const Cg<W> ap = load_cg<W>(io.ba, base + n, io.bnw), bp = load_cg<W>(io.bb, base + n, io.bnw);
-    const Cg<W> cg = load_cg<W>(io.bc, base, io.bnw), cp = load_cg<W>(io.bc, base + n, io.bnw);
-    Cg<W> o[4];
-    K::level_open(p0, l, Gc, P, ag, bg, ap, bp, o);
 #pragma unroll
-    for (int s = 0; s < 4; ++s) put_pk(buf, s * PW, o[s]);
+  for (int l = 0; l < L; ++l) {
+    const int buf = (l + 1) & 1, sg = 1 + 2 * l, sp = 2 + 2 * l;
+    Cg<W> o[4];
+    K::level_open(p0, l, Gc, P, ta[sg], tbv[sg], ta[sp], tbv[sp], o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) put_pk(buf, q * PW, o[q]);
     __syncthreads();
-    const Cg<W> zg = K::and_z(p0, o[0] ^ get_pk(buf, 0), o[2] ^ get_pk(buf, 2 * PW), ag, bg, cg);
-    const Cg<W> zp = K::and_z(p0, o[1] ^ get_pk(buf, PW), o[3] ^ get_pk(buf, 3 * PW), ap, bp, cp);
+    const Cg<W> zg = K::and_z(p0, o[0] ^ get_pk(buf, 0), o[2] ^ get_pk(buf, 2 * PW), ta[sg], tbv[sg], tc[sg]);
+    const Cg<W> zp = K::and_z(p0, o[1] ^ get_pk(buf, PW), o[3] ^ get_pk(buf, 3 * PW), ta[sp], tbv[sp], tc[sp]);
     Gc = Gc ^ zg;
     P = zp;
   }
 
   // ---- round L+1: B2A of the sign bit on Z/2^N
-  const unsigned sg = K::sign_bits(S, Gc);
-  const u64 ta = io.acur + e0;
+  const unsigned sgn = K::sign_bits(S, Gc);
   u64 d[GS];
   {
-    const int buf = (K::L + 1) & 1;
-    u64 a1[GS], b1[GS], e1[GS], f1[GS];
+    const int buf = (L + 1) & 1;
+    u64 e1[GS], f1[GS];
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      a1[j] = (j < valid) ? io.aa[ta + j] : 0ull;
-      b1[j] = (j < valid) ? io.ab[ta + j] : 0ull;
-      const u64 bit = (sg >> j) & 1u;
-      const u64 u = p0 ? bit : 0ull, v = p0 ? 0ull : bit;
-      e1[j] = (u - a1[j]) & MN;
-      f1[j] = (v - b1[j]) & MN;
+      const u64 bit = (sgn >> j) & 1u;
+      e1[j] = ((p0 ? bit : 0ull) - a1[j]) & MN;
+      f1[j] = ((p0 ? 0ull : bit) - b1[j]) & MN;
       slot(buf, party, j) = e1[j];
       slot(buf, party, GS + j) = f1[j];
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      const u64 c1 = (j < valid) ? io.ac[ta + j] : 0ull;
       const u64 E = (e1[j] + slot(buf, party ^ 1, j)) & MN;
       const u64 F = (f1[j] + slot(buf, party ^ 1, GS + j)) & MN;
-      const u64 tt = mul_z(p0, E, F, a1[j], b1[j], c1, MN);
-      const u64 bit = (sg >> j) & 1u;
-      const u64 lifted = (bit - 2 * tt) & MN;  // u + v = bit on exactly one party
-      d[j] = ((p0 ? 1ull : 0ull) - lifted) & MN;
+      const u64 tt = mul_z(p0, E, F, a1[j], b1[j], c1[j], MN);
+      const u64 bit = (sgn >> j) & 1u;
+      d[j] = ((p0 ? 1ull : 0ull) - ((bit - 2 * tt) & MN)) & MN;  // u + v = bit on one party
     }
   }
-  if (A.drelu_only) {
-#pragma unroll
-    for (int j = 0; j < GS; ++j)
-      if (j < valid) io.y[e0 + j] = d[j];
+  if (!mult) {
+    store_u64s<GS>(io.y + e0, valid, d);
     return;
   }
 
   // ---- round L+2: y = MUL(x, d)
   {
-    const int buf = K::L & 1;
-    u64 a2[GS], b2[GS], e2[GS], f2[GS];
+    const int buf = L & 1;
+    u64 e2[GS], f2[GS], yv[GS];
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      a2[j] = (j < valid) ? io.aa[ta + n + j] : 0ull;
-      b2[j] = (j < valid) ? io.ab[ta + n + j] : 0ull;
       e2[j] = (x[j] - a2[j]) & MN;
       f2[j] = (d[j] - b2[j]) & MN;
       slot(buf, party, j) = e2[j];
@@ -244,12 +248,11 @@ __global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      const u64 c2 = (j < valid) ? io.ac[ta + n + j] : 0ull;
       const u64 E = (e2[j] + slot(buf, party ^ 1, j)) & MN;
       const u64 F = (f2[j] + slot(buf, party ^ 1, GS + j)) & MN;
-      const u64 yv = mul_z(p0, E, F, a2[j], b2[j], c2, MN);
-      if (j < valid) io.y[e0 + j] = yv;
+      yv[j] = mul_z(p0, E, F, a2[j], b2[j], c2[j], MN);
     }
+    store_u64s<GS>(io.y + e0, valid, yv);
   }
 }
 
@@ -306,6 +309,36 @@ HB_DEV u64 get_arith(const u64* s, u64 idx, int N) {
   u64 v = s[b >> 6] >> sh;
   if (sh + N > 64) v |= s[(b >> 6) + 1] << (64 - sh);
   return v & nmask(N);
+}
+
+// A group's two arithmetic openings [e | f] at stream positions e0.. and n+e0..
+template <int GS>
+HB_DEV void put_arith_group(u64* own, u64 e0, u64 n, int valid, const u64 (&e)[GS], const u64 (&f)[GS], int N) {
+  if (N == 64) {
+    store_u64s<GS>(own + e0, valid, e);
+    store_u64s<GS>(own + n + e0, valid, f);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < GS; ++j)
+    if (j < valid) {
+      put_arith(own, e0 + j, e[j], N);
+      put_arith(own, n + e0 + j, f[j], N);
+    }
+}
+
+template <int GS>
+HB_DEV void get_arith_group(const u64* peer, u64 e0, u64 n, int valid, u64 (&e)[GS], u64 (&f)[GS], int N) {
+  if (N == 64) {
+    load_u64s<GS>(peer + e0, valid, e);
+    load_u64s<GS>(peer + n + e0, valid, f);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < GS; ++j) {
+    e[j] = (j < valid) ? get_arith(peer, e0 + j, N) : 0ull;
+    f[j] = (j < valid) ? get_arith(peer, n + e0 + j, N) : 0ull;
+  }
 }
 
 // round kinds of the staged driver (round index r):
@@ -393,47 +426,63 @@ __global__ void __launch_bounds__(256) k_stage(const StageArgs A) {
     stage_combine_bool<W>(A, g, e0, p0, Gc, P);
     const unsigned sg = K::sign_bits(ws_load<W>(A.S, g, ng), Gc);
     A.sign[g] = sg;
+    u64 a[GS], b[GS], e[GS], f[GS];
+    load_u64s<GS>(io.aa + ta, valid, a);
+    load_u64s<GS>(io.ab + ta, valid, b);
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      if (j < valid) {
-        const u64 bit = (sg >> j) & 1u;
-        put_arith(A.own, e0 + j, ((p0 ? bit : 0ull) - io.aa[ta + j]) & MN, A.N);
-        put_arith(A.own, n + e0 + j, ((p0 ? 0ull : bit) - io.ab[ta + j]) & MN, A.N);
-      }
+      const u64 bit = (sg >> j) & 1u;
+      e[j] = ((p0 ? bit : 0ull) - a[j]) & MN;
+      f[j] = ((p0 ? 0ull : bit) - b[j]) & MN;
     }
+    put_arith_group<GS>(A.own, e0, n, valid, e, f, A.N);
   } else if constexpr (KIND == RK_MULT) {
     const unsigned sg = A.sign[g];
+    u64 a[GS], b[GS], c[GS], pe[GS], pf[GS], d[GS];
+    load_u64s<GS>(io.aa + ta, valid, a);
+    load_u64s<GS>(io.ab + ta, valid, b);
+    load_u64s<GS>(io.ac + ta, valid, c);
+    get_arith_group<GS>(A.peer, e0, n, valid, pe, pf, A.N);
+    u64 x[GS], a2[GS], b2[GS];
+    if (!A.drelu_only) {
+      load_u64s<GS>(io.x + e0, valid, x);
+      load_u64s<GS>(io.aa + ta + n, valid, a2);
+      load_u64s<GS>(io.ab + ta + n, valid, b2);
+    }
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      if (j < valid) {
-        const u64 bit = (sg >> j) & 1u;
-        const u64 a = io.aa[ta + j], b = io.ab[ta + j], c = io.ac[ta + j];
-        const u64 e = ((p0 ? bit : 0ull) - a) & MN, f = ((p0 ? 0ull : bit) - b) & MN;
-        const u64 E = (e + get_arith(A.peer, e0 + j, A.N)) & MN;
-        const u64 F = (f + get_arith(A.peer, n + e0 + j, A.N)) & MN;
-        const u64 tt = mul_z(p0, E, F, a, b, c, MN);
-        const u64 d = ((p0 ? 1ull : 0ull) - ((bit - 2 * tt) & MN)) & MN;
-        if (A.drelu_only) {
-          io.y[e0 + j] = d;
-        } else {
-          A.d[e0 + j] = d;
-          const u64 x = io.x[e0 + j];
-          put_arith(A.own, e0 + j, (x - io.aa[ta + n + j]) & MN, A.N);
-          put_arith(A.own, n + e0 + j, (d - io.ab[ta + n + j]) & MN, A.N);
-        }
+      const u64 bit = (sg >> j) & 1u;
+      const u64 E = (((p0 ? bit : 0ull) - a[j]) + pe[j]) & MN;
+      const u64 F = (((p0 ? 0ull : bit) - b[j]) + pf[j]) & MN;
+      const u64 tt = mul_z(p0, E, F, a[j], b[j], c[j], MN);
+      d[j] = ((p0 ? 1ull : 0ull) - ((bit - 2 * tt) & MN)) & MN;
+    }
+    if (A.drelu_only) {
+      store_u64s<GS>(io.y + e0, valid, d);
+    } else {
+      store_u64s<GS>(A.d + e0, valid, d);
+      u64 e2[GS], f2[GS];
+#pragma unroll
+      for (int j = 0; j < GS; ++j) {
+        e2[j] = (x[j] - a2[j]) & MN;
+        f2[j] = (d[j] - b2[j]) & MN;
       }
+      put_arith_group<GS>(A.own, e0, n, valid, e2, f2, A.N);
     }
   } else {  // RK_FINAL
+    u64 a[GS], b[GS], c[GS], x[GS], d[GS], pe[GS], pf[GS], y[GS];
+    load_u64s<GS>(io.aa + ta + n, valid, a);
+    load_u64s<GS>(io.ab + ta + n, valid, b);
+    load_u64s<GS>(io.ac + ta + n, valid, c);
+    load_u64s<GS>(io.x + e0, valid, x);
+    load_u64s<GS>(A.d + e0, valid, d);
+    get_arith_group<GS>(A.peer, e0, n, valid, pe, pf, A.N);
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
-      if (j < valid) {
-        const u64 a = io.aa[ta + n + j], b = io.ab[ta + n + j], c = io.ac[ta + n + j];
-        const u64 e = (io.x[e0 + j] - a) & MN, f = (A.d[e0 + j] - b) & MN;
-        const u64 E = (e + get_arith(A.peer, e0 + j, A.N)) & MN;
-        const u64 F = (f + get_arith(A.peer, n + e0 + j, A.N)) & MN;
-        io.y[e0 + j] = mul_z(p0, E, F, a, b, c, MN);
-      }
+      const u64 E = ((x[j] - a[j]) + pe[j]) & MN, F = ((d[j] - b[j]) + pf[j]) & MN;
+      y[j] = mul_z(p0, E, F, a[j], b[j], c[j], MN);
     }
+    store_u64s<GS>(io.y + e0, valid, y);
   }
 }
 

@@ -135,6 +135,36 @@ def deal_on_device(kind: str, width: int, count: int, seed: int, device=None):
     return (a ^ ra, b ^ rb, c ^ rc), (ra, rb, rc)
 
 
+def stock_on_device(stores, parties, kind: str, width: int, count: int, seed: int, chunk: int = 1 << 25) -> None:
+    """Stock `count` triples of one (kind, width) into each store (store i holds party
+    parties[i]'s share), generated chunk by chunk in HBM with deal_on_device and packed
+    straight into the final stream -- peak scratch is one chunk, not the whole stock.
+    Ranks that each hold one party call this with the same seed and get matching shares."""
+    dev = _dev.device()
+    chunk = max(64, (chunk // 64) * 64)  # whole 64-bit words per chunk for any width
+    if kind == BOOL:
+        words = (count * width + 63) // 64
+        outs = [[torch.zeros(max(words, 1), dtype=torch.int64, device=dev) for _ in range(3)] for _ in stores]
+    else:
+        outs = [[torch.empty(max(count, 1), dtype=torch.int64, device=dev) for _ in range(3)] for _ in stores]
+    for i, lo in enumerate(range(0, count, chunk)):
+        c = min(chunk, count - lo)
+        shares = deal_on_device(kind, width, c, seed * 100003 + i, dev)
+        for out, p in zip(outs, parties):
+            for dst, src in zip(out, shares[p]):
+                if kind == BOOL:
+                    w0 = lo * width // 64
+                    nw = (c * width + 63) // 64
+                    _lib.call("hb_pack", src.data_ptr(), c, width, dst[w0:w0 + nw].data_ptr(), _dev.stream_handle())
+                else:
+                    dst[lo:lo + c].copy_(src)
+        del shares
+    for st, out in zip(stores, outs):
+        if (kind, width) in st._streams:
+            raise ConfigError("stream already stocked")
+        st._streams[(kind, width)] = _DevStream(kind, width, count, *out)
+
+
 # ------------------------------------------------------------------ device store
 @dataclass
 class TripleView:
