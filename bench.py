@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sweep", default=None, help="write a (n, w) sweep table to this JSON file")
     p.add_argument("--triple-gb", type=float, default=64.0, help="HBM budget for stocked triples")
+    p.add_argument("--workload", choices=["relu", "resnet18", "resnet50"], default="relu")
+    p.add_argument("--batch", type=int, default=None, help="ResNet batch (default 512 / 128)")
+    p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                   help="N>1 exchange backend (gloo lets 2 ranks share one GPU for testing)")
     return p.parse_args()
 
 
@@ -303,6 +307,71 @@ def run_single(args):
     }
 
 
+# ------------------------------------------------------------------ ResNet private inference (N = 1)
+def run_resnet(args):
+    """ResNet private inference samples/s, both parties time-sliced on one GPU (BASELINE configs[2,3])."""
+    import torch
+
+    from paper_2309_04875_b200 import dealer, models, nn, transport
+    from paper_2309_04875_b200.protocol import ProtocolSession
+    from paper_2309_04875_b200.ring import BitWindow
+    from paper_2309_04875_b200.sharing import ArithShareTensor
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    if args.workload == "resnet18":
+        model, batch, shape = models.resnet18_cifar(0), args.batch or 512, (3, 32, 32)
+    else:
+        model, batch, shape = models.resnet50(0), args.batch or 128, (3, 64, 64)
+    win = BitWindow(args.k, args.m)
+    cfg = models.resnet_relu_config(model, win)
+    need = nn.triple_requirements(model, cfg, batch)
+    eps = transport.local_pair()
+    stores = (dealer.TripleStore(0), dealer.TripleStore(1))
+    for i, ((kind, width), count) in enumerate(sorted(need.items())):
+        dealer.stock_on_device(stores, (0, 1), kind, width, count, seed=500 + i)
+    sessions = (ProtocolSession(eps[0], stores[0], model.fixed_point), ProtocolSession(eps[1], stores[1], model.fixed_point))
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    x_f = torch.rand((batch,) + shape, generator=g, device=dev, dtype=torch.float64)
+    enc = torch.floor(x_f * 65536.0 + 0.5).to(torch.int64)
+    r = torch.empty_like(enc).random_(generator=g)
+    x0, x1 = ArithShareTensor(0, 64, enc + r), ArithShareTensor(1, 64, -r)
+    s = torch.cuda.current_stream()
+
+    def fwd():
+        for st in stores:
+            for (kind, width) in need:
+                st.rewind(kind, width)
+        return nn.model_forward_pair(sessions, x0, x1, model, cfg)
+
+    for _ in range(args.warmup):
+        y0, y1 = fwd()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        a.record(s)
+        for _ in range(args.steps):
+            y0, y1 = fwd()
+        b.record(s)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    relu_elems = sum(c for _, c in model.relu_sites()) * batch
+    logits_ok = bool(torch.isfinite((y0.data + y1.data).double()).all().item())
+    return {
+        "metric": f"{args.workload}_private_inference_samples_per_s", "value": batch / (ms / 1e3),
+        "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} private inference, batch {batch}, input {shape}, "
+                               f"all ReLU groups window ({args.k},{args.m})", "batch": batch,
+                   "relu_elements_per_forward": relu_elems, "parties": "1 pair time-sliced on 1 GPU",
+                   "path": "nn.model_forward_pair: int8-limb ring GEMM (cuBLASLt) + fused pair ReLU kernel",
+                   "weights": "random init (torchvision scheme), BN folded", "parallelism": "pair"},
+        "relu_elems_per_s_in_model": relu_elems / (ms / 1e3), "logits_finite": logits_ok, "clocks": clk.summary(),
+    }
+
+
 # ------------------------------------------------------------------ N > 1: party pairs over NCCL
 def run_multi(args):
     import torch
@@ -314,10 +383,14 @@ def run_multi(args):
     from paper_2309_04875_b200.sharing import ArithShareTensor
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    dist.init_process_group("nccl", device_id=dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+        args.triple_gb = min(args.triple_gb, 16.0)
     pairs = world // 2
     pair, party = rank // 2, rank % 2
     active = pair < pairs
@@ -343,9 +416,10 @@ def run_multi(args):
             store.rewind(dealer.ARITH, N)
         return protocol.relu(sess, ArithShareTensor(party, N, mine), win)
 
+    y = None
     if active:
         for _ in range(args.warmup):
-            step()
+            y = step()
     torch.cuda.synchronize()
     dist.barrier()
     with ClockSampler(local) as clk:
@@ -355,13 +429,25 @@ def run_multi(args):
         a.record(s)
         if active:
             for _ in range(args.steps):
-                step()
+                y = step()
         b.record(s)
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([a.elapsed_time(b)], device=dev)
+    ms = torch.tensor([a.elapsed_time(b)], device=dev if args.backend == "nccl" else "cpu")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
+    # correctness (untimed): partners swap a sample of x / y shares, party 0 reconstructs
+    ok = torch.ones(1, device=ms.device)
+    if active:
+        c = min(n, 1 << 20)
+        mine_s = torch.cat([mine[:c], y.data.reshape(-1)[:c]])
+        theirs = ep._swap(mine_s)
+        if not isinstance(theirs, torch.Tensor):
+            theirs = torch.from_numpy(np.frombuffer(theirs, dtype=np.int64).copy())
+        theirs = theirs.to(dev)
+        if party == 0:
+            ok[0] = float(check_sample(mine_s[:c], theirs[:c], mine_s[c:], theirs[c:], N, k, m))
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     out = None
     if rank == 0:
         value = pairs * n * args.steps / (total_ms / 1e3)
@@ -371,9 +457,9 @@ def run_multi(args):
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"secure ReLU layer n=2^{args.logn} per pair, window ({k},{m}) w={w}, N={N}",
                        "n_per_pair": n, "pairs": pairs, "window": [k, m], "ring_bits": N,
-                       "path": "staged hb_relu_round + NCCL send/recv per round (ranks 2i<->2i+1)",
+                       "path": f"staged hb_relu_round + {args.backend} send/recv per round (ranks 2i<->2i+1)",
                        "parallelism": f"{pairs} party pairs"},
-            "gpu_launches": args.steps * (L + 4), "clocks": clk.summary(),
+            "gpu_launches": args.steps * (L + 4), "clocks": clk.summary(), "correct": bool(ok.item() > 0.5),
             "e2e": None,
         }
     dist.destroy_process_group()
@@ -447,6 +533,8 @@ def main():
     elif args.sweep:
         run_sweep(args)
         return
+    elif args.workload != "relu":
+        out = run_resnet(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
         out = run_multi(args)
     else:

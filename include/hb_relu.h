@@ -125,6 +125,30 @@ int hb_ewise(int op, int party, int w, int64_t count, int p, const uint64_t* a, 
 /* 1 if any word > 1 (b2a_bit precondition, protocol.py:166-167); synchronises `stream` */
 int hb_any_above_one(const uint64_t* a, int64_t count, int* result, void* stream);
 
+/* ---- ring-exact linear layers on Z/2^64 shares (nn.py:198-259), SURVEY 8(f)-1 ----
+ * (X W^T) mod 2^64 = sum_{i+j<=7} 256^(i+j) x_i w_j^T with x_i the 8 byte limbs of the
+ * share and w_j the J balanced signed byte limbs of the encoded weight; every x_i w_j^T
+ * is an exact int8 x int8 -> int32 tensor-core GEMM over A = [x_i - 128] stacked along M.
+ *
+ * hb_im2col_limbs: share NCHW [batch, channels, height, width] (or [batch, K] with
+ *   1x1 geometry) -> out int8 [8][M][k_padded], M = batch*OH*OW, column k = c*kh*kw +
+ *   ki*kw + kj (the reference im2col order, nn.py:177-195), value = limb_i - 128.
+ * hb_limb_combine: products int32 [8*m][j_limbs*n_padded] (row i*m + mm, column
+ *   j*n_padded + nn; colsum [j_limbs][n_padded]) -> out uint64 = local truncation by
+ *   frac_bits (nn.py:198-211) of sum_{i+j<=7} (P + 128 colsum[j][nn]) << 8(i+j), plus bias[nn] on party 0
+ *   (nn.py:224).  layout 0: out[mm*n + nn]; layout 1 (conv): out[(b*n + nn)*spatial + s]
+ *   with mm = b*spatial + s (nn.py:242-243).
+ * hb_avgpool: window sum, times `inv` = encode(1/(kh*kw)), truncation (nn.py:246-259).
+ * hb_add_shares: out = a + b mod 2^64 (residual add, sharing.py:118-122). */
+int hb_im2col_limbs(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                    int pad, int64_t k_padded, int8_t* out, void* stream);
+int hb_limb_combine(const int32_t* products, int64_t m, int64_t n, int64_t n_padded, int j_limbs,
+                    const int32_t* colsum, int party, int frac_bits, const uint64_t* bias, int layout, int64_t spatial,
+                    uint64_t* out, void* stream);
+int hb_avgpool(const uint64_t* x, int64_t batch_channels, int height, int width, int kh, int kw, int stride,
+               uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream);
+int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

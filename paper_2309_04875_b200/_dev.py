@@ -46,7 +46,14 @@ def to_device(a, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
 def to_host(t: torch.Tensor, like) -> object:
     """Return `t` in the caller's representation (numpy for numpy inputs)."""
     if isinstance(like, torch.Tensor):
-        return t if like.is_cuda else t.cpu()
+        if like.is_cuda:
+            return t
+        if like.is_pinned():
+            out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            out.copy_(t, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return out
+        return t.cpu()
     return t.cpu().numpy().view(np.uint64)
 
 

@@ -19,7 +19,7 @@ from .errors import (
     TripleExhaustedError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhbrelu.so")
+LIB_PATH = os.environ.get("HB_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhbrelu.so")
 
 HB_OK, HB_ERR_CUDA, HB_ERR_CONFIG, HB_ERR_TRANSPORT, HB_ERR_DATA, HB_ERR_TRIPLES = range(6)
 TAG_BY_CODE = {0: "Circuit", 1: "Mult", 2: "B2A", 3: "Other"}
@@ -74,6 +74,13 @@ _SIGS = {
     "hb_ewise": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, u64p, u64p,
                                 u64p, u64p, ctypes.c_void_p]),
     "hb_any_above_one": (ctypes.c_int, [u64p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.c_void_p]),
+    "hb_im2col_limbs": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [ctypes.c_int64, u64p, ctypes.c_void_p]),
+    "hb_limb_combine": (ctypes.c_int, [u64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, u64p,
+                                       ctypes.c_int,
+                                       ctypes.c_int, u64p, ctypes.c_int, ctypes.c_int64, u64p, ctypes.c_void_p]),
+    "hb_avgpool": (ctypes.c_int, [u64p, ctypes.c_int64] + [ctypes.c_int] * 5 + [ctypes.c_uint64, ctypes.c_int,
+                                                                                  ctypes.c_int, u64p, ctypes.c_void_p]),
+    "hb_add_shares": (ctypes.c_int, [u64p, u64p, ctypes.c_int64, u64p, ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -40,6 +40,15 @@ cudaError_t hb_ops_ewise(int op, int party, int w, u64 n, int p, const u64* a, c
                          cudaStream_t s);
 cudaError_t hb_ops_any_gt1(const u64* a, u64 n, int* flag_dev, cudaStream_t s);
 
+// ---- ring linear-layer kernels (hb_ring.cu)
+cudaError_t hb_ring_limbs_im2col(const u64* x, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
+                                 long long Kp, int8_t* A, cudaStream_t s);
+cudaError_t hb_ring_combine(const int32_t* P, long long M, long long N, long long Np, int J, const int32_t* colsum,
+                            int party, int frac, const u64* bias, int layout, long long S, u64* out, cudaStream_t s);
+cudaError_t hb_ring_avgpool(const u64* x, long long BC, int H, int W, int kh, int kw, int stride, u64 inv, int party,
+                            int frac, u64* out, cudaStream_t s);
+cudaError_t hb_ring_add(const u64* a, const u64* b, long long n, u64* out, cudaStream_t s);
+
 namespace {
 
 thread_local std::string g_err;
@@ -362,6 +371,42 @@ int hb_any_above_one(const uint64_t* a, int64_t count, int* result, void* stream
   if (e != cudaSuccess) return cuda_status(e, "hb_any_above_one");
   *result = host;
   return HB_OK;
+}
+
+int hb_im2col_limbs(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                    int pad, int64_t k_padded, int8_t* out, void* stream) {
+  if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
+    return fail(HB_ERR_CONFIG, "bad conv geometry");
+  if (k_padded < (int64_t)channels * kh * kw) return fail(HB_ERR_CONFIG, "k_padded smaller than C*kh*kw");
+  if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
+  return cuda_status(hb_ring_limbs_im2col(x, batch, channels, height, width, kh, kw, stride, pad, k_padded, out,
+                                          S(stream)),
+                     "hb_im2col_limbs");
+}
+
+int hb_limb_combine(const int32_t* products, int64_t m, int64_t n, int64_t n_padded, int j_limbs,
+                    const int32_t* colsum, int party, int frac_bits, const uint64_t* bias, int layout, int64_t spatial,
+                    uint64_t* out, void* stream) {
+  if (n_padded < n) return fail(HB_ERR_CONFIG, "n_padded < n");
+  if (j_limbs < 1 || j_limbs > 8) return fail(HB_ERR_CONFIG, "weight limbs must be in 1..8");
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  if (frac_bits < 0 || frac_bits >= 64) return fail(HB_ERR_CONFIG, "frac_bits must be in 0..63");
+  if (layout == 1 && (spatial <= 0 || m % spatial)) return fail(HB_ERR_CONFIG, "spatial must divide m");
+  return cuda_status(hb_ring_combine(products, m, n, n_padded, j_limbs, colsum, party, frac_bits, bias, layout,
+                                     spatial, out, S(stream)),
+                     "hb_limb_combine");
+}
+
+int hb_avgpool(const uint64_t* x, int64_t batch_channels, int height, int width, int kh, int kw, int stride,
+               uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream) {
+  if (kh <= 0 || kw <= 0 || stride <= 0 || kh > height || kw > width) return fail(HB_ERR_CONFIG, "bad pool geometry");
+  return cuda_status(hb_ring_avgpool(x, batch_channels, height, width, kh, kw, stride, inv, party, frac_bits, out,
+                                     S(stream)),
+                     "hb_avgpool");
+}
+
+int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream) {
+  return cuda_status(hb_ring_add(a, b, n, out, S(stream)), "hb_add_shares");
 }
 
 }  // extern "C"

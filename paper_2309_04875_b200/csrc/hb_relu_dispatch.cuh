@@ -6,27 +6,36 @@
 
 namespace hb {
 
-constexpr int PAIR_TP = 128;  // threads per party per CTA (CTA = 2 * PAIR_TP)
+#ifndef HB_PAIR_TP
+#define HB_PAIR_TP 64
+#endif
+constexpr int PAIR_TP = HB_PAIR_TP;  // threads per party per CTA (CTA = 2 * PAIR_TP)
 
 template <int W>
 size_t pair_smem_bytes() {
   return sizeof(u64) * 2 * 2 * PairGeo<W>::SEGW * PAIR_TP;
 }
 
-template <int W>
-cudaError_t launch_pair(const PairArgs& A, cudaStream_t s) {
+template <int W, bool R64>
+cudaError_t launch_pair_impl(const PairArgs& A, cudaStream_t s) {
   constexpr int GS = Geo<W>::GS;
   const u64 ngroups = (A.n + GS - 1) / GS;
   const u64 blocks = (ngroups + PAIR_TP - 1) / PAIR_TP;
   const size_t smem = pair_smem_bytes<W>();
   static bool configured = false;  // benign race: idempotent attribute set
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_relu_pair<W, PAIR_TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_relu_pair<W, PAIR_TP, R64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_relu_pair<W, PAIR_TP><<<(unsigned)blocks, 2 * PAIR_TP, smem, s>>>(A);
+  k_relu_pair<W, PAIR_TP, R64><<<(unsigned)blocks, 2 * PAIR_TP, smem, s>>>(A);
   return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t launch_pair(const PairArgs& A, cudaStream_t s) {
+  return A.N == 64 ? launch_pair_impl<W, true>(A, s) : launch_pair_impl<W, false>(A, s);
 }
 
 template <int W>

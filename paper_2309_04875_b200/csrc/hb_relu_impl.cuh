@@ -121,8 +121,11 @@ struct PairGeo {
   static constexpr int SEGW = (4 * PW > 2 * GS) ? 4 * PW : 2 * GS;  // words per thread per wire buffer
 };
 
-template <int W, int TP>
-__global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
+#ifndef HB_PAIR_MINB
+#define HB_PAIR_MINB 1
+#endif
+template <int W, int TP, bool RING64>
+__global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairArgs A) {
   using G = Geo<W>;
   using K = Kit<W>;
   constexpr int GS = G::GS, PW = G::PW, SEGW = PairGeo<W>::SEGW, L = K::L, NSEG = 1 + 2 * L;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(2 * TP) k_relu_pair(const PairArgs A) {
   const u64 e0 = ((u64)blockIdx.x * TP + t) * GS;
   const int valid = e0 >= n ? 0 : (int)min((u64)GS, n - e0);
   const PartyIO& io = A.io[party];
-  const u64 MN = nmask(A.N);
+  const u64 MN = RING64 ? ~0ull : nmask(A.N);  // Z/2^64: masks fold away at compile time
   const bool mult = !A.drelu_only;
 
   auto slot = [&](int buf, int who, int k) -> u64& { return wire[((buf * 2 + who) * SEGW + k) * TP + t]; };

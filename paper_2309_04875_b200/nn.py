@@ -1,0 +1,555 @@
+"""Fixed-point layers over shares and the model-level private-inference entry.
+
+Same layer vocabulary, manifest JSON and semantics as the reference
+(ringmpc nn.py:33-174, 198-325) -- Linear, Conv2d, AvgPool, Relu, Flatten --
+plus ``Residual`` (out = body(x) + shortcut(x)), which ResNets need and the
+reference lacks.  Every layer runs on the GPU:
+
+* Linear / Conv2d: ring-exact (X W^T) mod 2^64 on int8 tensor cores.  The share
+  is split into 8 byte limbs by a fused im2col kernel (hb_im2col_limbs), the
+  encoded weight into J balanced signed byte limbs (once per model), ONE int8
+  GEMM produces every limb product (cuBLASLt via torch._int_mm, s8 x s8 ->
+  s32), and hb_limb_combine folds the products mod 2^64 together with the local
+  truncation, the party-0 bias and the NCHW layout.  Bit-identical to the
+  reference's uint64 numpy matmul (nn.py:214-243).
+* AvgPool: hb_avgpool (window sum, * encode(1/kk), truncation; nn.py:246-259).
+* Relu: ``protocol.relu`` (one party, any endpoint) or, for both parties on one
+  GPU, ``protocol.relu_pair`` (model_forward_pair / run_local_forward).
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _dev, _lib, dealer, protocol, ring, sharing, transport
+from .errors import ConfigError, DataFormatError
+from .protocol import ProtocolSession
+from .ring import BitWindow, FixedPointConfig
+from .sharing import ArithShareTensor
+
+
+# ------------------------------------------------------------------ layer vocabulary (nn.py:33-74)
+@dataclass(frozen=True)
+class Linear:
+    in_features: int
+    out_features: int
+    weight: str
+    bias: str
+    kind: str = field(default="linear", init=False)
+
+
+@dataclass(frozen=True)
+class Conv2d:
+    in_channels: int
+    out_channels: int
+    kh: int
+    kw: int
+    stride: int
+    pad: int
+    weight: str
+    bias: str
+    kind: str = field(default="conv2d", init=False)
+
+
+@dataclass(frozen=True)
+class AvgPool:
+    kh: int
+    kw: int
+    stride: int
+    kind: str = field(default="avgpool", init=False)
+
+
+@dataclass(frozen=True)
+class Relu:
+    group_id: int
+    kind: str = field(default="relu", init=False)
+
+
+@dataclass(frozen=True)
+class Flatten:
+    kind: str = field(default="flatten", init=False)
+
+
+@dataclass(frozen=True)
+class Residual:
+    """out = body(x) + shortcut(x) (empty shortcut = identity); a local add of shares."""
+
+    body: tuple
+    shortcut: tuple = ()
+    kind: str = field(default="residual", init=False)
+
+
+def _walk(layers):
+    for L in layers:
+        yield L
+        if isinstance(L, Residual):
+            yield from _walk(L.body)
+            yield from _walk(L.shortcut)
+
+
+def _out_shape(layers, cur):
+    for L in layers:
+        cur = _layer_shape(L, cur)
+    return cur
+
+
+def _layer_shape(L, cur):
+    if isinstance(L, Linear):
+        if cur != (L.in_features,):
+            raise ConfigError(f"linear layer expects ({L.in_features},), got {cur}")
+        return (L.out_features,)
+    if isinstance(L, Conv2d):
+        if len(cur) != 3 or cur[0] != L.in_channels:
+            raise ConfigError(f"conv layer expects ({L.in_channels}, H, W), got {cur}")
+        _, h, w = cur
+        return (L.out_channels, (h + 2 * L.pad - L.kh) // L.stride + 1, (w + 2 * L.pad - L.kw) // L.stride + 1)
+    if isinstance(L, AvgPool):
+        if len(cur) != 3:
+            raise ConfigError(f"avgpool expects (C, H, W), got {cur}")
+        c, h, w = cur
+        return (c, (h - L.kh) // L.stride + 1, (w - L.kw) // L.stride + 1)
+    if isinstance(L, Flatten):
+        return (int(np.prod(cur)),)
+    if isinstance(L, Residual):
+        a, b = _out_shape(L.body, cur), _out_shape(L.shortcut, cur)
+        if a != b:
+            raise ConfigError(f"residual branches disagree: {a} vs {b}")
+        return a
+    return cur  # Relu
+
+
+@dataclass
+class ModelSpec:
+    """Layers + public float32 weights (nn.py:77-145)."""
+
+    fixed_point: FixedPointConfig
+    input_shape: tuple
+    layers: list
+    weights: dict
+
+    def __post_init__(self) -> None:
+        groups = [L.group_id for L in _walk(self.layers) if isinstance(L, Relu)]
+        if sorted(set(groups)) != list(range(len(set(groups)))):
+            raise ConfigError(f"relu group ids must cover 0..G-1, got {groups}")
+        for L in _walk(self.layers):
+            if isinstance(L, Linear):
+                self._expect(L.weight, (L.out_features, L.in_features))
+                self._expect(L.bias, (L.out_features,))
+            elif isinstance(L, Conv2d):
+                self._expect(L.weight, (L.out_channels, L.in_channels, L.kh, L.kw))
+                self._expect(L.bias, (L.out_channels,))
+        self.activation_shapes()
+
+    def _expect(self, name, shape):
+        if name not in self.weights:
+            raise ConfigError(f"missing weight blob {name!r}")
+        if tuple(self.weights[name].shape) != tuple(shape):
+            raise ConfigError(f"blob {name!r} has shape {self.weights[name].shape}, expected {shape}")
+
+    @property
+    def n_groups(self) -> int:
+        return len({L.group_id for L in _walk(self.layers) if isinstance(L, Relu)})
+
+    def activation_shapes(self) -> list:
+        shapes, cur = [tuple(self.input_shape)], tuple(self.input_shape)
+        for L in self.layers:
+            cur = _layer_shape(L, cur)
+            shapes.append(cur)
+        return shapes
+
+    def relu_sites(self):
+        """(group_id, per-sample element count) of every ReLU, in execution order."""
+        out = []
+
+        def visit(layers, cur):
+            for L in layers:
+                if isinstance(L, Relu):
+                    out.append((L.group_id, int(np.prod(cur))))
+                elif isinstance(L, Residual):
+                    visit(L.body, cur)
+                    visit(L.shortcut, cur)
+                cur = _layer_shape(L, cur)
+
+        visit(self.layers, tuple(self.input_shape))
+        return out
+
+    def relu_group_sizes(self) -> dict:
+        sizes = {}
+        for g, c in self.relu_sites():
+            sizes[g] = sizes.get(g, 0) + c
+        return sizes
+
+
+@dataclass
+class ReluConfig:
+    """Per-group window or None (identity) (nn.py:148-174)."""
+
+    windows: list
+
+    @classmethod
+    def full(cls, model: ModelSpec) -> "ReluConfig":
+        return cls([BitWindow(model.fixed_point.ring_bits, 0)] * model.n_groups)
+
+    def window_for(self, group_id: int):
+        if not 0 <= group_id < len(self.windows):
+            raise ConfigError(f"no window configured for relu group {group_id}")
+        return self.windows[group_id]
+
+    def to_json(self) -> dict:
+        return {"groups": [w.to_json() if w is not None else "identity" for w in self.windows]}
+
+    @classmethod
+    def from_json(cls, obj: dict) -> "ReluConfig":
+        return cls([None if e == "identity" else BitWindow.from_json(e) for e in obj["groups"]])
+
+
+# ------------------------------------------------------------------ ring GEMM (int8 limbs)
+@dataclass
+class _LimbWeight:
+    """Encoded weight W [N, K] as J balanced byte limbs, ready for the int8 GEMM."""
+
+    n: int
+    k: int
+    kp: int
+    np_: int
+    j: int
+    bt: torch.Tensor      # int8 [J*Np, Kp]  (row j*Np + n = limb j of W[n, :])
+    colsum: torch.Tensor  # int32 [J, Np]
+    bias: torch.Tensor    # uint64 (int64) [Np] encoded bias
+
+
+def _balanced_limbs(w: np.ndarray):
+    """W = sum_j l_j 256^j with l_j in [-128, 127]; returns the list of limbs."""
+    rem = w.astype(np.int64).copy()
+    limbs = []
+    while np.any(rem != 0) or not limbs:
+        l = ((rem + 128) & 255) - 128
+        limbs.append(l.astype(np.int8))
+        rem = (rem - l) >> 8
+        if len(limbs) > 8:
+            raise ConfigError("weight limbs do not terminate")
+    return limbs
+
+
+def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) -> _LimbWeight:
+    w_enc = ring.to_signed(ring.encode_array(np.asarray(weight, dtype=np.float64), cfg), 64)
+    n, k = w_enc.shape
+    kp, np_ = -(-k // 16) * 16, -(-n // 8) * 8
+    limbs = _balanced_limbs(w_enc)
+    j = len(limbs)
+    bt = np.zeros((j, np_, kp), dtype=np.int8)
+    for jj, l in enumerate(limbs):
+        bt[jj, :n, :k] = l
+    colsum = bt.astype(np.int32).sum(axis=2, dtype=np.int32)  # the kernel reads int32
+    b = np.zeros(np_, dtype=np.uint64)
+    b[:n] = ring.encode_array(np.asarray(bias, dtype=np.float64), cfg)
+    dev = _dev.device()
+    return _LimbWeight(n, k, kp, np_, j, torch.from_numpy(bt.reshape(j * np_, kp)).to(dev),
+                       torch.from_numpy(colsum).to(dev), torch.from_numpy(b.view(np.int64)).to(dev))
+
+
+_WCACHE: dict = {}
+
+
+def _weight(weight, bias, cfg) -> _LimbWeight:
+    """Limb form of a layer's weight, prepared once per weight array (public data)."""
+    key = (id(weight), id(bias), cfg)
+    hit = _WCACHE.get(key)
+    if hit is None or hit[0] is not weight or hit[1] is not bias:
+        hit = (weight, bias, _prep_weight(np.asarray(weight).reshape(weight.shape[0], -1), bias, cfg))
+        _WCACHE[key] = hit
+    return hit[2]
+
+
+def _ring_gemm(xd: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int, layout: int, spatial: int):
+    """One party's (patches(x) @ W^T) mod 2^64 -> truncate -> + bias, on the GPU."""
+    b, c, h, w, kh, kw, stride, pad = geom
+    oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    m = b * oh * ow
+    s = _dev.stream_handle()
+    a = torch.empty((8 * m, lw.kp), dtype=torch.int8, device=xd.device)
+    _lib.call("hb_im2col_limbs", xd.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.kp, a.data_ptr(), s)
+    if 8 * m <= 16:  # the int8 GEMM needs more than 16 rows; padded rows are ignored
+        a = torch.cat([a, torch.zeros((24 - 8 * m, lw.kp), dtype=torch.int8, device=a.device)])
+    prod = torch._int_mm(a, lw.bt.t())  # [8m(+pad), J*Np] int32 -- tensor cores
+    out = torch.empty(m * lw.n, dtype=torch.int64, device=xd.device)
+    _lib.call("hb_limb_combine", prod.data_ptr(), m, lw.n, lw.np_, lw.j, lw.colsum.data_ptr(), party, frac,
+              lw.bias.data_ptr() if party == 0 else None, layout, spatial, out.data_ptr(), s)
+    return out
+
+
+def _check_ring(x, cfg):
+    if x.width != 64 or cfg.ring_bits != 64:
+        raise ConfigError("GPU ring layers run on Z/2^64 shares (FixedPointConfig(ring_bits=64))")
+
+
+def truncate_local(x: ArithShareTensor, cfg: FixedPointConfig) -> ArithShareTensor:
+    """Local SecureML truncation (nn.py:198-211), on the GPU."""
+    _check_ring(x, cfg)
+    xd = _dev.to_device(x.data).reshape(-1)
+    out = torch.empty_like(xd)
+    # the avgpool kernel with a 1x1 window and inv = 1 is exactly the truncation
+    _lib.call("hb_avgpool", xd.data_ptr(), xd.numel(), 1, 1, 1, 1, 1, 1, x.party, cfg.frac_bits, out.data_ptr(),
+              _dev.stream_handle())
+    return ArithShareTensor(x.party, x.width, _dev.to_host(out.reshape(x.shape), x.data))
+
+
+def linear_forward(session: ProtocolSession, x: ArithShareTensor, weight, bias) -> ArithShareTensor:
+    """x @ W^T + b with public fixed-point weights; no communication (nn.py:214-224)."""
+    cfg = session.fxp
+    _check_ring(x, cfg)
+    if len(x.shape) != 2 or x.shape[1] != weight.shape[1]:
+        raise ConfigError(f"linear expects [batch, {weight.shape[1]}], got {x.shape}")
+    lw = _weight(weight, bias, cfg)
+    xd = _dev.to_device(x.data)
+    b, k = x.shape
+    out = _ring_gemm(xd, (b, k, 1, 1, 1, 1, 1, 0), lw, x.party, cfg.frac_bits, 0, 1)
+    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, lw.n), x.data))
+
+
+def conv2d_forward(session: ProtocolSession, x: ArithShareTensor, layer: Conv2d, weight, bias) -> ArithShareTensor:
+    """Convolution as fused im2col + ring GEMM (nn.py:227-243)."""
+    cfg = session.fxp
+    _check_ring(x, cfg)
+    if len(x.shape) != 4 or x.shape[1] != layer.in_channels:
+        raise ConfigError(f"conv expects [batch, {layer.in_channels}, H, W], got {x.shape}")
+    lw = _weight(weight, bias, cfg)
+    xd = _dev.to_device(x.data)
+    b, c, h, w = x.shape
+    oh, ow = (h + 2 * layer.pad - layer.kh) // layer.stride + 1, (w + 2 * layer.pad - layer.kw) // layer.stride + 1
+    out = _ring_gemm(xd, (b, c, h, w, layer.kh, layer.kw, layer.stride, layer.pad), lw, x.party, cfg.frac_bits, 1,
+                     oh * ow)
+    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, layer.out_channels, oh, ow), x.data))
+
+
+def avgpool_forward(session: ProtocolSession, x: ArithShareTensor, layer: AvgPool) -> ArithShareTensor:
+    """Window sum, * encode(1/kk), truncation (nn.py:246-259)."""
+    cfg = session.fxp
+    _check_ring(x, cfg)
+    if len(x.shape) != 4:
+        raise ConfigError(f"avgpool expects [batch, C, H, W], got {x.shape}")
+    b, c, h, w = x.shape
+    oh, ow = (h - layer.kh) // layer.stride + 1, (w - layer.kw) // layer.stride + 1
+    inv = ring.encode_fixed(1.0 / (layer.kh * layer.kw), cfg).value
+    xd = _dev.to_device(x.data)
+    out = torch.empty(b * c * oh * ow, dtype=torch.int64, device=xd.device)
+    _lib.call("hb_avgpool", xd.data_ptr(), b * c, h, w, layer.kh, layer.kw, layer.stride, inv, x.party,
+              cfg.frac_bits, out.data_ptr(), _dev.stream_handle())
+    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, c, oh, ow), x.data))
+
+
+def relu_forward(session: ProtocolSession, x: ArithShareTensor, window) -> ArithShareTensor:
+    """Windowed ReLU; None is the identity with no rounds (nn.py:262-268)."""
+    return x if window is None else protocol.relu(session, x, window)
+
+
+def _add(a: ArithShareTensor, b: ArithShareTensor) -> ArithShareTensor:
+    ad, bd = _dev.to_device(a.data), _dev.to_device(b.data)
+    out = torch.empty_like(ad)
+    _lib.call("hb_add_shares", ad.data_ptr(), bd.data_ptr(), ad.numel(), out.data_ptr(), _dev.stream_handle())
+    return ArithShareTensor(a.party, a.width, _dev.to_host(out, a.data))
+
+
+def _local_layer(session, cur, L, model):
+    if isinstance(L, Linear):
+        return linear_forward(session, cur, model.weights[L.weight], model.weights[L.bias])
+    if isinstance(L, Conv2d):
+        return conv2d_forward(session, cur, L, model.weights[L.weight], model.weights[L.bias])
+    if isinstance(L, AvgPool):
+        return avgpool_forward(session, cur, L)
+    if isinstance(L, Flatten):
+        return ArithShareTensor(cur.party, cur.width, cur.data.reshape(cur.shape[0], -1))
+    raise ConfigError(f"unknown layer kind {L!r}")
+
+
+def _meter_delta(ep, before):
+    after = ep.meter.snapshot()
+    return sum(after[t][0] - before[t][0] for t in after), sum(after[t][1] - before[t][1] for t in after)
+
+
+def model_forward(session: ProtocolSession, x: ArithShareTensor, model: ModelSpec, relu_cfg: ReluConfig,
+                  layer_meter: list | None = None) -> ArithShareTensor:
+    """One party runs every layer (nn.py:271-307); shares stay on the GPU between layers."""
+    if len(relu_cfg.windows) != model.n_groups:
+        raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
+
+    def run(layers, cur, prefix):
+        for i, L in enumerate(layers):
+            before = session.endpoint.meter.snapshot()
+            if isinstance(L, Relu):
+                cur = relu_forward(session, cur, relu_cfg.window_for(L.group_id))
+            elif isinstance(L, Residual):
+                cur = _add(run(L.body, cur, f"{prefix}{i}.body."), run(L.shortcut, cur, f"{prefix}{i}.short."))
+            else:
+                cur = _local_layer(session, cur, L, model)
+            if layer_meter is not None:
+                nb, nr = _meter_delta(session.endpoint, before)
+                layer_meter.append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
+        return cur
+
+    host_in = x.data
+    cur = ArithShareTensor(x.party, x.width, _dev.to_device(x.data))
+    out = run(model.layers, cur, "")
+    return ArithShareTensor(out.party, out.width, _dev.to_host(out.data, host_in))
+
+
+def model_forward_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, model: ModelSpec,
+                       relu_cfg: ReluConfig, layer_meter: tuple | None = None):
+    """Both parties on this GPU: local layers per party, every ReLU through the fused
+    pair kernel (protocol.relu_pair).  Same shares and meters as two model_forward threads."""
+    if len(relu_cfg.windows) != model.n_groups:
+        raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
+    s0, s1 = sessions
+
+    def run(layers, c0, c1, prefix):
+        for i, L in enumerate(layers):
+            b0, b1 = s0.endpoint.meter.snapshot(), s1.endpoint.meter.snapshot()
+            if isinstance(L, Relu):
+                win = relu_cfg.window_for(L.group_id)
+                if win is not None:
+                    c0, c1 = protocol.relu_pair((s0, s1), c0, c1, win)
+            elif isinstance(L, Residual):
+                a0, a1 = run(L.body, c0, c1, f"{prefix}{i}.body.")
+                h0, h1 = run(L.shortcut, c0, c1, f"{prefix}{i}.short.")
+                c0, c1 = _add(a0, h0), _add(a1, h1)
+            else:
+                c0, c1 = _local_layer(s0, c0, L, model), _local_layer(s1, c1, L, model)
+            if layer_meter is not None:
+                for p, (s, bef) in enumerate(((s0, b0), (s1, b1))):
+                    nb, nr = _meter_delta(s.endpoint, bef)
+                    layer_meter[p].append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
+        return c0, c1
+
+    d0 = ArithShareTensor(0, x0.width, _dev.to_device(x0.data))
+    d1 = ArithShareTensor(1, x1.width, _dev.to_device(x1.data))
+    o0, o1 = run(model.layers, d0, d1, "")
+    return (ArithShareTensor(0, o0.width, _dev.to_host(o0.data, x0.data)),
+            ArithShareTensor(1, o1.width, _dev.to_host(o1.data, x1.data)))
+
+
+def triple_requirements(model: ModelSpec, relu_cfg: ReluConfig, batch: int) -> dict:
+    """(kind, width) -> count for one forward pass (nn.py:310-325)."""
+    need = {}
+    for g, count in model.relu_sites():
+        win = relu_cfg.window_for(g)
+        if win is None:
+            continue
+        for key, num in protocol.relu_triple_cost(count * batch, win.width, model.fixed_point.ring_bits).items():
+            need[key] = need.get(key, 0) + num
+    return need
+
+
+# ------------------------------------------------------------------ model-level entry (cli.py:159-180)
+_INPUT_STREAM = 0x1289
+
+
+def _seed_rng(seed: int, *scope: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence([seed, *scope]))
+
+
+def _triple_seed(seed: int, kind: str, width: int) -> int:
+    code = 1 if kind == dealer.ARITH else 2
+    return int(np.random.SeedSequence([seed, 0x7337, code, width]).generate_state(1)[0])
+
+
+def build_stores(model: ModelSpec, relu_cfg: ReluConfig, batch: int, seed: int):
+    """Both parties' stores dealt from the run seed, as the reference CLI does (cli.py:40-58)."""
+    stores = (dealer.TripleStore(0), dealer.TripleStore(1))
+    for (kind, width), count in sorted(triple_requirements(model, relu_cfg, batch).items()):
+        gen = dealer.gen_arith_triples if kind == dealer.ARITH else dealer.gen_bool_triples
+        b = gen(count, width, _triple_seed(seed, kind, width))
+        for st in stores:
+            st.add_batch(b)
+    return stores
+
+
+def run_local_forward(model: ModelSpec, relu_cfg: ReluConfig, x_f, seed: int, pair: bool = True):
+    """Both parties in process -> (logits, (meter0, meter1), layer_logs, wall_ms) (cli.py:159-180).
+
+    pair=True runs the parties time-sliced on this GPU (fused ReLU kernel);
+    pair=False runs two party threads over a LocalEndpoint, as the reference does."""
+    cfg = model.fixed_point
+    enc = ring.encode_array(x_f, cfg)
+    s0, s1 = sharing.share_arith(enc, cfg.ring_bits, _seed_rng(seed, _INPUT_STREAM))
+    stores = build_stores(model, relu_cfg, x_f.shape[0], seed)
+    ep0, ep1 = transport.local_pair()
+    sessions = (ProtocolSession(ep0, stores[0], cfg), ProtocolSession(ep1, stores[1], cfg))
+    logs: tuple = ([], [])
+    torch.cuda.synchronize()
+    start = time.perf_counter()
+    if pair:
+        o0, o1 = model_forward_pair(sessions, s0, s1, model, relu_cfg, logs)
+    else:
+        o0, o1 = transport.run_parties(lambda: model_forward(sessions[0], s0, model, relu_cfg, logs[0]),
+                                       lambda: model_forward(sessions[1], s1, model, relu_cfg, logs[1]),
+                                       endpoints=(ep0, ep1))
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - start) * 1e3
+    logits = ring.decode_array(sharing.reconstruct_arith(o0, o1), cfg)
+    return logits, (ep0.meter, ep1.meter), logs, wall_ms
+
+
+# ------------------------------------------------------------------ manifest I/O (nn.py:372-455)
+def _layer_to_json(L) -> dict:
+    out = {"kind": L.kind}
+    for k, v in L.__dict__.items():
+        if k == "kind":
+            continue
+        out[k] = [_layer_to_json(c) for c in v] if k in ("body", "shortcut") else v
+    return out
+
+
+def _layer_from_json(obj: dict):
+    kinds = {"linear": Linear, "conv2d": Conv2d, "avgpool": AvgPool, "relu": Relu, "flatten": Flatten,
+             "residual": Residual}
+    try:
+        cls = kinds[obj["kind"]]
+        kw = {k: v for k, v in obj.items() if k != "kind"}
+        if cls is Residual:
+            kw = {k: tuple(_layer_from_json(c) for c in kw.get(k, ())) for k in ("body", "shortcut")}
+        return cls(**kw)
+    except (KeyError, TypeError) as exc:
+        raise DataFormatError(f"bad layer entry {obj!r}: {exc}") from exc
+
+
+def save_model(model: ModelSpec, out_dir) -> None:
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    blobs = {}
+    for name, arr in model.weights.items():
+        fname = name.replace(".", "_") + ".bin"
+        (out / fname).write_bytes(np.asarray(arr, dtype="<f4").tobytes())
+        blobs[name] = fname
+    manifest = {"fixed_point": model.fixed_point.to_json(), "input_shape": list(model.input_shape),
+                "layers": [_layer_to_json(L) for L in model.layers], "blobs": blobs}
+    (out / "manifest.json").write_text(json.dumps(manifest, indent=2))
+
+
+def load_model(path) -> ModelSpec:
+    p = Path(path)
+    if p.is_dir():
+        p = p / "manifest.json"
+    try:
+        man = json.loads(p.read_text())
+        fxp = FixedPointConfig.from_json(man["fixed_point"])
+        layers = [_layer_from_json(o) for o in man["layers"]]
+        shapes = {}
+        for L in _walk(layers):
+            if isinstance(L, Linear):
+                shapes[L.weight], shapes[L.bias] = (L.out_features, L.in_features), (L.out_features,)
+            elif isinstance(L, Conv2d):
+                shapes[L.weight] = (L.out_channels, L.in_channels, L.kh, L.kw)
+                shapes[L.bias] = (L.out_channels,)
+        weights = {}
+        for name, fname in man["blobs"].items():
+            raw = np.frombuffer((p.parent / fname).read_bytes(), dtype="<f4")
+            weights[name] = raw.reshape(shapes.get(name, raw.shape)).astype(np.float32)
+        return ModelSpec(fxp, tuple(man["input_shape"]), layers, weights)
+    except (OSError, KeyError, TypeError, ValueError) as exc:
+        raise DataFormatError(f"{p}: malformed model: {exc}") from exc

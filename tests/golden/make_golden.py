@@ -202,6 +202,42 @@ def main():
         dl[f"{kind}_{w}_{seed}_{cnt}"] = [sha(a) for p_ in (0, 1) for a in b.party_arrays(p_)]
     META["dealer_streams"] = dl
 
+    # ---------------- ring linear layers (nn.py:198-259), per party
+    from ringmpc import models, nn
+    from ringmpc.cli import run_local_forward
+
+    class _Sess:  # the layer functions only read session.fxp
+        fxp = FixedPointConfig(64, 16)
+
+    for case in gc.NN_CASES:
+        ins = gc.make_nn_inputs(case)
+        outs = []
+        for party in (0, 1):
+            x = sharing.ArithShareTensor(party, 64, ins[f"x{party}"])
+            if case["op"] == "linear":
+                r = nn.linear_forward(_Sess, x, ins["w"], ins["b"])
+            elif case["op"] == "conv":
+                r = nn.conv2d_forward(_Sess, x, nn.Conv2d(*case["layer"], weight="w", bias="b"), ins["w"], ins["b"])
+            elif case["op"] == "avgpool":
+                r = nn.avgpool_forward(_Sess, x, nn.AvgPool(*case["layer"]))
+            else:
+                r = nn.truncate_local(x, _Sess.fxp)
+            outs.append(np.asarray(r.data, dtype=np.uint64))
+        META[case["name"]] = {"y0_sha": sha(outs[0]), "y1_sha": sha(outs[1]), "shape": list(outs[0].shape)}
+
+    # ---------------- model-level entry: run_local_forward (cli.py:159-180) on desk models
+    for mc in gc.MODEL_CASES:
+        model = models.build_cnn(11) if mc["arch"] == "cnn" else models.build_mlp(11)
+        for name, arr in model.weights.items():
+            ARR[f"model_{mc['arch']}/{name}"] = arr
+        x_f = gc.model_inputs(mc)
+        cfg = nn.ReluConfig([None if w is None else BitWindow(*w) for w in mc["windows"]])
+        logits, meters, logs, _ = run_local_forward(model, cfg, x_f, mc["seed"])
+        META[mc["name"]] = {"logits_sha": sha(np.ascontiguousarray(logits).view(np.uint64)),
+                            "meter0": meters[0].to_json(), "meter1": meters[1].to_json(),
+                            "layers0": logs[0], "layers1": logs[1]}
+        ARR[mc["name"] + "/logits"] = logits
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **ARR)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(META, fh, indent=1, sort_keys=True)

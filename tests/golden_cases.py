@@ -201,3 +201,64 @@ def make_stage_inputs(case):
     if r == "b2a":
         return dict(x0=np.array([0, 0, 1, 1], dtype=U64), x1=np.array([0, 1, 0, 1], dtype=U64))
     raise KeyError(r)
+
+
+# ------------------------------------------------------------------ ring linear layers (nn.py:198-259)
+NN_CASES = [
+    dict(name="nn_linear", op="linear", x_shape=(12, 40), w_shape=(24, 40)),
+    dict(name="nn_linear_big", op="linear", x_shape=(33, 300), w_shape=(10, 300), w_scale=3.0),
+    dict(name="nn_conv", op="conv", x_shape=(3, 5, 9, 9), w_shape=(7, 5, 3, 3), layer=(5, 7, 3, 3, 2, 1)),
+    dict(name="nn_conv_1x1", op="conv", x_shape=(2, 6, 8, 8), w_shape=(4, 6, 1, 1), layer=(6, 4, 1, 1, 2, 0)),
+    dict(name="nn_conv_stem", op="conv", x_shape=(2, 3, 8, 8), w_shape=(16, 3, 3, 3), layer=(3, 16, 3, 3, 1, 1)),
+    dict(name="nn_avgpool", op="avgpool", x_shape=(3, 7, 8, 8), layer=(2, 2, 2)),
+    dict(name="nn_avgpool_4", op="avgpool", x_shape=(2, 5, 8, 8), layer=(4, 4, 4)),
+    dict(name="nn_truncate", op="truncate", x_shape=(1000,)),
+]
+
+
+def make_nn_inputs(case):
+    """Shares of encoded N(0, 4^2) activations and N(0, 0.2^2) weights (seeded by the case name)."""
+    seed = sum(ord(ch) for ch in case["name"])
+    rng = np.random.default_rng(seed)
+    x_f = rng.normal(0, 4.0, case["x_shape"])
+    x0, x1 = share_arith(encode(x_f), 64, rng)
+    out = dict(x0=x0, x1=x1)
+    if "w_shape" in case:
+        out["w"] = (rng.normal(0, 0.2 * case.get("w_scale", 1.0), case["w_shape"])).astype(np.float32)
+        out["b"] = rng.normal(0, 0.5, case["w_shape"][0]).astype(np.float32)
+    return out
+
+
+MODEL_CASES = [
+    dict(name="model_cnn_full", arch="cnn", windows=[(64, 0), (64, 0)], seed=5, batch=16),
+    dict(name="model_cnn_reduced", arch="cnn", windows=[(20, 8), (19, 6)], seed=5, batch=16),
+    dict(name="model_cnn_identity", arch="cnn", windows=[None, (22, 14)], seed=7, batch=8),
+    dict(name="model_mlp_reduced", arch="mlp", windows=[(21, 13)], seed=3, batch=32),
+]
+
+
+def model_inputs(mc):
+    rng = np.random.default_rng(77 + mc["batch"])
+    shape = (mc["batch"], 1, 8, 8) if mc["arch"] == "cnn" else (mc["batch"], 64)
+    return rng.uniform(0.0, 1.0, shape)
+
+
+def _conv(cin, cout, k, stride, pad, w, b):
+    return dict(kind="conv2d", in_channels=cin, out_channels=cout, kh=k, kw=k, stride=stride, pad=pad, weight=w, bias=b)
+
+
+# layer lists of the reference desk models (models.py:33-72), as manifest JSON entries (nn.py:440-455)
+MODEL_LAYERS = {
+    "cnn": ([_conv(1, 8, 3, 1, 1, "conv1.w", "conv1.b"), dict(kind="relu", group_id=0),
+             dict(kind="avgpool", kh=2, kw=2, stride=2), _conv(8, 16, 3, 1, 1, "conv2.w", "conv2.b"),
+             dict(kind="relu", group_id=1), dict(kind="avgpool", kh=2, kw=2, stride=2), dict(kind="flatten"),
+             dict(kind="linear", in_features=64, out_features=10, weight="fc.w", bias="fc.b")], (1, 8, 8)),
+    "mlp": ([dict(kind="linear", in_features=64, out_features=32, weight="fc1.w", bias="fc1.b"),
+             dict(kind="relu", group_id=0),
+             dict(kind="linear", in_features=32, out_features=10, weight="fc2.w", bias="fc2.b")], (64,)),
+}
+
+
+def model_weights(arrays, arch):
+    pre = f"model_{arch}/"
+    return {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}

@@ -1,0 +1,137 @@
+"""GPU parity of the ring linear layers and the model-level entry.
+
+Bar: bit-exact.  Layer outputs per party equal the reference's nn.linear_forward /
+conv2d_forward / avgpool_forward / truncate_local on the same shares (golden
+digests); run_local_forward reproduces the reference's logits SHA, meters and
+per-layer logs on its desk models; ResNet-shaped models (residual blocks, which
+the reference cannot express) match the oracle share for share.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_cases as gc
+from hb_helpers import sha
+from oracle import hb_oracle as O
+from oracle import hb_oracle_nn as ON
+from paper_2309_04875_b200 import models, nn
+from paper_2309_04875_b200.ring import BitWindow, FixedPointConfig
+from paper_2309_04875_b200.sharing import ArithShareTensor
+
+pytestmark = pytest.mark.gpu
+
+
+class _Sess:
+    fxp = FixedPointConfig(64, 16)
+
+
+@pytest.mark.parametrize("case", gc.NN_CASES, ids=[c["name"] for c in gc.NN_CASES])
+def test_nn_layer_golden(golden, case):
+    g = golden[0][case["name"]]
+    ins = gc.make_nn_inputs(case)
+    for p in (0, 1):
+        x = ArithShareTensor(p, 64, ins[f"x{p}"])
+        if case["op"] == "linear":
+            y = nn.linear_forward(_Sess, x, ins["w"], ins["b"])
+        elif case["op"] == "conv":
+            y = nn.conv2d_forward(_Sess, x, nn.Conv2d(*case["layer"], weight="w", bias="b"), ins["w"], ins["b"])
+        elif case["op"] == "avgpool":
+            y = nn.avgpool_forward(_Sess, x, nn.AvgPool(*case["layer"]))
+        else:
+            y = nn.truncate_local(x, _Sess.fxp)
+        assert list(y.shape) == g["shape"]
+        assert sha(y.data) == g[f"y{p}_sha"], (case["name"], p)
+
+
+def _desk(arch, arrays):
+    m = models.desk_cnn(11) if arch == "cnn" else models.desk_mlp(11)
+    for k, v in gc.model_weights(arrays, arch).items():  # the reference's own draws
+        assert np.array_equal(m.weights[k], v), k
+    return m
+
+
+@pytest.mark.parametrize("pair", [True, False], ids=["pair", "threads"])
+@pytest.mark.parametrize("mc", gc.MODEL_CASES, ids=[c["name"] for c in gc.MODEL_CASES])
+def test_run_local_forward_golden(golden, mc, pair):
+    meta, arrays = golden
+    g = meta[mc["name"]]
+    model = _desk(mc["arch"], arrays)
+    cfg = nn.ReluConfig([None if w is None else BitWindow(*w) for w in mc["windows"]])
+    logits, meters, logs, _ = nn.run_local_forward(model, cfg, gc.model_inputs(mc), mc["seed"], pair=pair)
+    assert O.digest(np.ascontiguousarray(logits).view(np.uint64)) == g["logits_sha"]
+    assert meters[0].to_json() == g["meter0"] and meters[1].to_json() == g["meter1"]
+    assert logs[0] == g["layers0"] and logs[1] == g["layers1"]
+
+
+def _tiny_resnet():
+    ini = models._Init(3)
+    layers = [ini.conv("stem", 3, 8, 3, 1, 1), nn.Relu(0)]
+    layers += models._basic_block(ini, "b1", 8, 8, 1, 1)
+    layers += models._basic_block(ini, "b2", 8, 16, 2, 2)
+    layers += models._bottleneck(ini, "b3", 16, 4, 1, 2)
+    layers += [nn.AvgPool(4, 4, 4), nn.Flatten(), ini.linear("fc", 16, 10)]
+    return nn.ModelSpec(FixedPointConfig(), (3, 8, 8), layers, ini.weights)
+
+
+@pytest.mark.parametrize("windows", [[(22, 14)] * 3, [(64, 0), (20, 6), None]], ids=["w8", "mixed"])
+def test_resnet_shaped_vs_oracle(windows):
+    model = _tiny_resnet()
+    x_f = np.random.default_rng(5).uniform(0, 1, (6, 3, 8, 8))
+    cfg = nn.ReluConfig([None if w is None else BitWindow(*w) for w in windows])
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    want, traces, wlogs = ON.run_local_forward(layers, model.input_shape, model.weights, windows, x_f, 9)
+    for pair in (True, False):
+        logits, meters, logs, _ = nn.run_local_forward(model, cfg, x_f, 9, pair=pair)
+        assert np.array_equal(logits, want)
+        assert logs[0] == wlogs[0]
+        assert [tuple(t) for t in meters[0].trace] == [tuple(t) for t in traces[0]]
+
+
+def test_resnet18_forward_smoke():
+    """Full ResNet18-CIFAR at batch 2: runs, spends the analytic rounds, and the logits
+    track the plaintext fixed-point forward (fidelity, not exactness: local truncation)."""
+    model = models.resnet18_cifar(0)
+    cfg = models.resnet_relu_config(model, BitWindow(64, 0))
+    x_f = np.random.default_rng(1).uniform(0, 1, (2, 3, 32, 32))
+    logits, meters, logs, _ = nn.run_local_forward(model, cfg, x_f, 3)
+    assert logits.shape == (2, 10) and np.all(np.isfinite(logits))
+    assert meters[0].rounds["Circuit"] == 6 * 17 and meters[0].rounds["Mult"] == 17
+    # float reference forward with the same weights (BN folded) and exact ReLU
+    ref = _float_forward(model, x_f)
+    assert np.max(np.abs(logits - ref)) < 0.05
+
+
+def _float_forward(model, x):
+    import torch.nn.functional as F
+
+    def run(layers, t):
+        for L in layers:
+            if isinstance(L, nn.Conv2d):
+                t = F.conv2d(t, torch.from_numpy(model.weights[L.weight]).double(),
+                             torch.from_numpy(model.weights[L.bias]).double(), L.stride, L.pad)
+            elif isinstance(L, nn.Relu):
+                t = torch.relu(t)
+            elif isinstance(L, nn.Residual):
+                t = run(L.body, t) + run(L.shortcut, t)
+            elif isinstance(L, nn.AvgPool):
+                t = F.avg_pool2d(t, (L.kh, L.kw), L.stride)
+            elif isinstance(L, nn.Flatten):
+                t = t.reshape(t.shape[0], -1)
+            elif isinstance(L, nn.Linear):
+                t = t @ torch.from_numpy(model.weights[L.weight]).double().T + torch.from_numpy(
+                    model.weights[L.bias]).double()
+        return t
+
+    return run(model.layers, torch.from_numpy(np.asarray(x, dtype=np.float64))).numpy()
+
+
+def test_limb_gemm_exact_at_resnet_width():
+    """The int8-limb ring GEMM equals uint64 numpy matmul at K = 4608 (ResNet18's largest)."""
+    rng = np.random.default_rng(2)
+    x = np.frombuffer(rng.bytes(8 * 40 * 4608), dtype="<u8").copy().reshape(40, 4608)
+    w = rng.normal(0, 0.05, (24, 4608)).astype(np.float32)
+    b = rng.normal(0, 0.1, 24).astype(np.float32)
+    for p in (0, 1):
+        y = nn.linear_forward(_Sess, ArithShareTensor(p, 64, x), w, b)
+        assert np.array_equal(y.data, ON.linear(x, p, w, b))

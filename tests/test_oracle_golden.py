@@ -134,3 +134,43 @@ def test_analytic_bytes_table():
     for w, want in ((64, 240), (32, 120), (16, 68), (8, 46), (6, 42.5)):
         tot = sum(nb for _, nb in O.analytic_trace(n, w, 64))
         assert tot / n == want
+
+
+# ------------------------------------------------------------------ ring layers / model level
+from oracle import hb_oracle_nn as ON  # noqa: E402
+
+
+def _nn_oracle(case, ins, party):
+    x = ins[f"x{party}"]
+    if case["op"] == "linear":
+        return ON.linear(x, party, ins["w"], ins["b"])
+    if case["op"] == "conv":
+        cin, cout, kh, kw, s, p = case["layer"]
+        return ON.conv2d(x, party, cin, cout, kh, kw, s, p, ins["w"], ins["b"])
+    if case["op"] == "avgpool":
+        return ON.avgpool(x, party, *case["layer"])
+    return ON.truncate(x, party)
+
+
+@pytest.mark.parametrize("case", gc.NN_CASES, ids=[c["name"] for c in gc.NN_CASES])
+def test_nn_layers(golden, case):
+    g = golden[0][case["name"]]
+    ins = gc.make_nn_inputs(case)
+    for p in (0, 1):
+        y = _nn_oracle(case, ins, p)
+        assert list(y.shape) == g["shape"]
+        assert O.digest(y) == g[f"y{p}_sha"]
+
+
+@pytest.mark.parametrize("mc", gc.MODEL_CASES, ids=[c["name"] for c in gc.MODEL_CASES])
+def test_model_run_local_forward(golden, mc):
+    meta, arrays = golden
+    g = meta[mc["name"]]
+    layers, in_shape = gc.MODEL_LAYERS[mc["arch"]]
+    weights = gc.model_weights(arrays, mc["arch"])
+    logits, traces, logs = ON.run_local_forward(layers, in_shape, weights, mc["windows"], gc.model_inputs(mc),
+                                                mc["seed"])
+    assert O.digest(np.ascontiguousarray(logits).view(np.uint64)) == g["logits_sha"]
+    assert logs[0] == g["layers0"] and logs[1] == g["layers1"]
+    tot = O.tag_totals(traces[0])
+    assert {t: {"bytes": tot[t][0], "rounds": tot[t][1]} for t in O.TAGS} == g["meter0"]["tags"]
