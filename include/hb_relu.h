@@ -149,6 +149,15 @@ int hb_avgpool(const uint64_t* x, int64_t batch_channels, int height, int width,
                uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream);
 int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream);
 
+/* Fused ring conv/linear on tcgen05 tensor cores (hand-written, sm_100a): im2col gather, byte-limb
+ * split, u8 x s8 -> s32 MMAs with the 8 byte-shift accumulators in TMEM, fold mod 2^64, local
+ * truncation, party-0 bias, NCHW store -- one kernel, no int32 intermediates in HBM.
+ * wlimbs: int8 [ceil(n_out/n_tile)][k_padded/64][j_limbs][n_tile x 64 UMMA canonical K-major tile];
+ * k_padded % 64 == 0, C*kh*kw <= 21900, j_limbs <= 3, n_tile in {16, 32, 64}. */
+int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                     int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,
+                     int frac_bits, const uint64_t* bias, uint64_t* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@
 
 #include "../../include/hb_relu.h"
 #include "hb_relu_impl.cuh"
+#include "hb_ring_tc.cuh"
 
 using hb::u64;
 
@@ -403,6 +404,44 @@ int hb_avgpool(const uint64_t* x, int64_t batch_channels, int height, int width,
   return cuda_status(hb_ring_avgpool(x, batch_channels, height, width, kh, kw, stride, inv, party, frac_bits, out,
                                      S(stream)),
                      "hb_avgpool");
+}
+
+int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                     int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,
+                     int frac_bits, const uint64_t* bias, uint64_t* y, void* stream) {
+  if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
+    return fail(HB_ERR_CONFIG, "bad conv geometry");
+  if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
+  const int64_t K = (int64_t)channels * kh * kw;
+  if (k_padded % 64 || k_padded < K) return fail(HB_ERR_CONFIG, "k_padded must be a multiple of 64 >= C*kh*kw");
+  if (K > 21900) return fail(HB_ERR_CONFIG, "K = %lld too large for exact int32 shift accumulators", (long long)K);
+  if (j_limbs < 1 || j_limbs > 3) return fail(HB_ERR_CONFIG, "tensor-core path supports 1..3 weight limbs");
+  if (n_tile != 16 && n_tile != 32 && n_tile != 64) return fail(HB_ERR_CONFIG, "n_tile must be 16, 32 or 64");
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  hb::tc::ConvArgs A;
+  A.x = x;
+  A.B = batch;
+  A.C = channels;
+  A.H = height;
+  A.W = width;
+  A.kh = kh;
+  A.kw = kw;
+  A.stride = stride;
+  A.pad = pad;
+  A.OH = (height + 2 * pad - kh) / stride + 1;
+  A.OW = (width + 2 * pad - kw) / stride + 1;
+  A.M = (long long)batch * A.OH * A.OW;
+  A.K = K;
+  A.Kp = (int)k_padded;
+  A.N = n_out;
+  A.J = j_limbs;
+  A.wl = wlimbs;
+  A.party = party;
+  A.frac = frac_bits;
+  A.bias = bias;
+  A.y = y;
+  if (A.M == 0) return HB_OK;
+  return cuda_status(hb_tc_conv(A, n_tile, S(stream)), "hb_conv_limbs_tc");
 }
 
 int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream) {

@@ -20,6 +20,7 @@ reference lacks.  Every layer runs on the GPU:
 from __future__ import annotations
 
 import json
+import os
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -222,6 +223,9 @@ class _LimbWeight:
     bt: torch.Tensor      # int8 [J*Np, Kp]  (row j*Np + n = limb j of W[n, :])
     colsum: torch.Tensor  # int32 [J, Np]
     bias: torch.Tensor    # uint64 (int64) [Np] encoded bias
+    wl_tc: torch.Tensor | None = None  # int8 tiles for hb_conv_limbs_tc (None: not eligible)
+    kp_tc: int = 0
+    nt: int = 0
 
 
 def _balanced_limbs(w: np.ndarray):
@@ -250,8 +254,25 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
     b = np.zeros(np_, dtype=np.uint64)
     b[:n] = ring.encode_array(np.asarray(bias, dtype=np.float64), cfg)
     dev = _dev.device()
-    return _LimbWeight(n, k, kp, np_, j, torch.from_numpy(bt.reshape(j * np_, kp)).to(dev),
-                       torch.from_numpy(colsum).to(dev), torch.from_numpy(b.view(np.int64)).to(dev))
+    lw = _LimbWeight(n, k, kp, np_, j, torch.from_numpy(bt.reshape(j * np_, kp)).to(dev),
+                     torch.from_numpy(colsum).to(dev), torch.from_numpy(b.view(np.int64)).to(dev))
+    if j <= 3 and k <= 21900:
+        lw.nt = 64 if n >= 64 else (32 if n > 16 else 16)
+        lw.kp_tc = -(-k // 64) * 64
+        lw.wl_tc = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt, lw.kp_tc)).to(dev)
+    return lw
+
+
+def _tc_tiles(limbs, n, k, nt, kp):
+    """Weight limbs in the tensor-core kernel's order [n tile][k block of 64][limb][UMMA canonical
+    K-major tile: (row>>3, k>>4, row&7, k&15)] (hb_ring_tc.cu)."""
+    j = len(limbs)
+    ntiles = -(-n // nt)
+    full = np.zeros((j, ntiles * nt, kp), dtype=np.int8)
+    for jj, l in enumerate(limbs):
+        full[jj, :n, :k] = l
+    t = full.reshape(j, ntiles, nt // 8, 8, kp // 64, 4, 16)        # j, tile, g, rr, kb, cc, e
+    return np.ascontiguousarray(t.transpose(1, 4, 0, 2, 5, 3, 6)).reshape(-1)  # tile, kb, j, g, cc, rr, e
 
 
 _WCACHE: dict = {}
@@ -267,12 +288,21 @@ def _weight(weight, bias, cfg) -> _LimbWeight:
     return hit[2]
 
 
+RING_GEMM = os.environ.get("HB_RING_GEMM", "tc")  # "tc" (hand-written tcgen05) or "cublaslt"
+
+
 def _ring_gemm(xd: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int, layout: int, spatial: int):
     """One party's (patches(x) @ W^T) mod 2^64 -> truncate -> + bias, on the GPU."""
     b, c, h, w, kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
     m = b * oh * ow
     s = _dev.stream_handle()
+    if RING_GEMM == "tc" and lw.wl_tc is not None:
+        # fused tcgen05 kernel: output is NCHW, which for linear (1x1 spatial) is [b, n]
+        out = torch.empty(m * lw.n, dtype=torch.int64, device=xd.device)
+        _lib.call("hb_conv_limbs_tc", xd.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n,
+                  lw.j, lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
+        return out
     a = torch.empty((8 * m, lw.kp), dtype=torch.int8, device=xd.device)
     _lib.call("hb_im2col_limbs", xd.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.kp, a.data_ptr(), s)
     if 8 * m <= 16:  # the int8 GEMM needs more than 16 rows; padded rows are ignored
