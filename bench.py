@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--path", choices=["pair", "staged"], default="pair", help="N=1 driver")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-resnet", action="store_true", help="skip the ResNet18 secondary measurement")
     p.add_argument("--sweep", default=None, help="write a (n, w) sweep table to this JSON file")
     p.add_argument("--triple-gb", type=float, default=64.0, help="HBM budget for stocked triples")
     p.add_argument("--workload", choices=["relu", "resnet18", "resnet50"], default="relu")
@@ -287,6 +288,17 @@ def run_single(args):
                "path": "protocol.relu_pair with pinned host shares in and host shares out", "steps": reps}
 
     cpu = None if args.no_cpu_baseline else cpu_baseline(k, m, N)
+    resnet = None
+    if not args.no_resnet and args.path == "pair" and args.logn == 24:
+        del stores, sessions, x0, x1, y0, y1
+        torch.cuda.empty_cache()
+        import copy
+
+        ra = copy.copy(args)
+        ra.workload, ra.batch, ra.steps, ra.warmup = "resnet18", 512, 3, 2
+        r = run_resnet(ra)
+        resnet = {"metric": r["metric"], "value": r["value"], "unit": r["unit"], "ms_per_step": r["ms_per_step"],
+                  "config": r["config"], "steps": r["steps"], "warmup": r["warmup"]}
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -304,6 +316,7 @@ def run_single(args):
                      "frac_vs_survey_H": (2 * n * bpe["survey_H"] / (launch_ms / 1e3) / 1e9) / peak,
                      "kernel": f"hb::k_relu_pair<{w},128>", "launch_ms": launch_ms},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+        "resnet18": resnet,
     }
 
 
@@ -366,7 +379,8 @@ def run_resnet(args):
         "config": {"workload": f"{args.workload} private inference, batch {batch}, input {shape}, "
                                f"all ReLU groups window ({args.k},{args.m})", "batch": batch,
                    "relu_elements_per_forward": relu_elems, "parties": "1 pair time-sliced on 1 GPU",
-                   "path": "nn.model_forward_pair: int8-limb ring GEMM (cuBLASLt) + fused pair ReLU kernel",
+                   "path": "nn.model_forward_pair: int8-limb ring conv ("
+                           + ("hand-written tcgen05 kernel" if nn.RING_GEMM == "tc" else "cuBLASLt") + ") + fused pair ReLU kernel",
                    "weights": "random init (torchvision scheme), BN folded", "parallelism": "pair"},
         "relu_elems_per_s_in_model": relu_elems / (ms / 1e3), "logits_finite": logits_ok, "clocks": clk.summary(),
     }
@@ -394,6 +408,8 @@ def run_multi(args):
     pairs = world // 2
     pair, party = rank // 2, rank % 2
     active = pair < pairs
+    if args.workload != "relu":
+        return run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active)
     n, k, m, N = 1 << args.logn, args.k, args.m, args.ring_bits
     w = k - m
     L = protocol.prefix_levels(w)
@@ -466,6 +482,80 @@ def run_multi(args):
     return out
 
 
+def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
+    """ResNet private inference on `pairs` party pairs (ranks 2i/2i+1), batch sharded over pairs
+    (BASELINE configs[4]: ResNet18 batch 4096 on 4 pairs).  Each rank runs nn.model_forward for
+    its party; every ReLU round is a send/recv with its partner rank."""
+    import torch
+
+    from paper_2309_04875_b200 import dealer, models, nn, transport
+    from paper_2309_04875_b200.protocol import ProtocolSession
+    from paper_2309_04875_b200.ring import BitWindow
+    from paper_2309_04875_b200.sharing import ArithShareTensor
+
+    if args.workload == "resnet18":
+        model, total, shape = models.resnet18_cifar(0), args.batch or 4096, (3, 32, 32)
+    else:
+        model, total, shape = models.resnet50(0), args.batch or 512, (3, 64, 64)
+    per_pair = max(1, total // max(pairs, 1))
+    cfg = models.resnet_relu_config(model, BitWindow(args.k, args.m))
+    s = torch.cuda.current_stream()
+    if active:
+        ep = transport.DistEndpoint(party, rank ^ 1)
+        store = dealer.TripleStore(party)
+        need = nn.triple_requirements(model, cfg, per_pair)
+        for i, ((kind, width), count) in enumerate(sorted(need.items())):
+            dealer.stock_on_device((store,), (party,), kind, width, count, seed=500 + 31 * pair + i)
+        sess = ProtocolSession(ep, store, model.fixed_point)
+        g = torch.Generator(device=dev)
+        g.manual_seed(7 + pair)  # both ranks of a pair derive the same split, keep their own share
+        x_f = torch.rand((per_pair,) + shape, generator=g, device=dev, dtype=torch.float64)
+        enc = torch.floor(x_f * 65536.0 + 0.5).to(torch.int64)
+        r = torch.empty_like(enc).random_(generator=g)
+        mine = ArithShareTensor(party, 64, enc + r if party == 0 else -r)
+        del x_f, enc, r
+
+    def fwd():
+        for (kind, width) in need:
+            store.rewind(kind, width)
+        return nn.model_forward(sess, mine, model, cfg)
+
+    if active:
+        for _ in range(args.warmup):
+            fwd()
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(dev.index) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record(s)
+        if active:
+            for _ in range(args.steps):
+                fwd()
+        b.record(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([a.elapsed_time(b)], device=dev if args.backend == "nccl" else "cpu")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    out = None
+    if rank == 0:
+        out = {
+            "metric": f"{args.workload}_private_inference_samples_per_s",
+            "value": pairs * per_pair * args.steps / (total_ms / 1e3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload} private inference, batch {pairs * per_pair} over {pairs} pairs",
+                       "batch": pairs * per_pair, "batch_per_pair": per_pair, "pairs": pairs,
+                       "path": f"nn.model_forward per party, staged ReLU + {args.backend} send/recv per round",
+                       "parallelism": f"{pairs} party pairs"},
+            "clocks": clk.summary(), "e2e": None,
+        }
+    dist.destroy_process_group()
+    return out
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     from oracle import hb_oracle as O
@@ -533,10 +623,10 @@ def main():
     elif args.sweep:
         run_sweep(args)
         return
-    elif args.workload != "relu":
-        out = run_resnet(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
         out = run_multi(args)
+    elif args.workload != "relu":
+        out = run_resnet(args)
     else:
         out = run_single(args)
     if out is not None:

@@ -148,11 +148,25 @@ int hb_limb_combine(const int32_t* products, int64_t m, int64_t n, int64_t n_pad
 int hb_avgpool(const uint64_t* x, int64_t batch_channels, int height, int width, int kh, int kw, int stride,
                uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream);
 int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream);
+/* hb_avgpool on NHWC shares: x [batch][height][width][channels] -> out [batch][OH][OW][channels] */
+int hb_avgpool_nhwc(const uint64_t* x, int64_t batch, int height, int width, int channels, int kh, int kw, int stride,
+                    uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream);
+
+/* ---- trusted dealer in HBM (dealer.py:50-83), bit-exact with gen_arith_triples /
+ * gen_bool_triples: (state, inc) = the 128-bit PCG64 state of default_rng(SeedSequence(seed)) before
+ * any draw (numpy bit_generator.state).  Writes triples [first, first + n) of a batch of `count`
+ * (both parties' a, b, c as uint64 residues of `width` bits).  kind 0 = arith, 1 = bool. */
+int hb_deal_triples(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int kind, int width,
+                    int64_t count, int64_t first, int64_t n, uint64_t* a0, uint64_t* b0, uint64_t* c0, uint64_t* a1,
+                    uint64_t* b1, uint64_t* c1, void* stream);
 
 /* Fused ring conv/linear on tcgen05 tensor cores (hand-written, sm_100a): im2col gather, byte-limb
  * split, u8 x s8 -> s32 MMAs with the 8 byte-shift accumulators in TMEM, fold mod 2^64, local
- * truncation, party-0 bias, NCHW store -- one kernel, no int32 intermediates in HBM.
- * wlimbs: int8 [ceil(n_out/n_tile)][k_padded/64][j_limbs][n_tile x 64 UMMA canonical K-major tile];
+ * truncation, party-0 bias -- one kernel, no int32 intermediates in HBM.
+ * Layouts are NHWC: x [batch][height][width][channels], y [batch][OH][OW][n_out] (a linear layer is
+ * the 1x1 case, x [batch][K]); patch index k = (ki*kw + kj)*channels + c.
+ * wlimbs: int8 [ceil(n_out/n_tile)][k_padded/64][j_limbs][n_tile x 64 UMMA canonical K-major tile],
+ * built from the weight permuted to [n_out][kh][kw][channels];
  * k_padded % 64 == 0, C*kh*kw <= 21900, j_limbs <= 3, n_tile in {16, 32, 64}. */
 int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
                      int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,

@@ -81,6 +81,12 @@ _SIGS = {
     "hb_avgpool": (ctypes.c_int, [u64p, ctypes.c_int64] + [ctypes.c_int] * 5 + [ctypes.c_uint64, ctypes.c_int,
                                                                                   ctypes.c_int, u64p, ctypes.c_void_p]),
     "hb_add_shares": (ctypes.c_int, [u64p, u64p, ctypes.c_int64, u64p, ctypes.c_void_p]),
+    "hb_avgpool_nhwc": (ctypes.c_int, [u64p, ctypes.c_int64] + [ctypes.c_int] * 6 + [ctypes.c_uint64, ctypes.c_int,
+                                                                                      ctypes.c_int, u64p,
+                                                                                      ctypes.c_void_p]),
+    "hb_deal_triples": (ctypes.c_int, [ctypes.c_uint64] * 4 + [ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                                                ctypes.c_int64, ctypes.c_int64] + [u64p] * 6
+                        + [ctypes.c_void_p]),
     "hb_conv_limbs_tc": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p,
                                                                         u64p, ctypes.c_void_p]),

@@ -40,6 +40,9 @@ cudaError_t hb_ops_open_close(int kind, int party, int w, u64 n, const u64* x, c
 cudaError_t hb_ops_ewise(int op, int party, int w, u64 n, int p, const u64* a, const u64* b, u64* out, u64* out2,
                          cudaStream_t s);
 cudaError_t hb_ops_any_gt1(const u64* a, u64 n, int* flag_dev, cudaStream_t s);
+cudaError_t hb_dealer_launch(uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, int kind, int width,
+                             unsigned long long count, unsigned long long first, unsigned long long n, uint64_t* a0,
+                             uint64_t* b0, uint64_t* c0, uint64_t* a1, uint64_t* b1, uint64_t* c1, cudaStream_t s);
 
 // ---- ring linear-layer kernels (hb_ring.cu)
 cudaError_t hb_ring_limbs_im2col(const u64* x, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
@@ -49,6 +52,8 @@ cudaError_t hb_ring_combine(const int32_t* P, long long M, long long N, long lon
 cudaError_t hb_ring_avgpool(const u64* x, long long BC, int H, int W, int kh, int kw, int stride, u64 inv, int party,
                             int frac, u64* out, cudaStream_t s);
 cudaError_t hb_ring_add(const u64* a, const u64* b, long long n, u64* out, cudaStream_t s);
+cudaError_t hb_ring_avgpool_nhwc(const u64* x, long long B, int H, int W, int C, int kh, int kw, int stride, u64 inv,
+                                 int party, int frac, u64* out, cudaStream_t s);
 
 namespace {
 
@@ -442,6 +447,27 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
   A.y = y;
   if (A.M == 0) return HB_OK;
   return cuda_status(hb_tc_conv(A, n_tile, S(stream)), "hb_conv_limbs_tc");
+}
+
+int hb_deal_triples(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int kind, int width,
+                    int64_t count, int64_t first, int64_t n, uint64_t* a0, uint64_t* b0, uint64_t* c0, uint64_t* a1,
+                    uint64_t* b1, uint64_t* c1, void* stream) {
+  if (kind != 0 && kind != 1) return fail(HB_ERR_CONFIG, "kind must be 0 (arith) or 1 (bool)");
+  if (width < 1 || width > 64) return fail(HB_ERR_CONFIG, "width must be in 1..64, got %d", width);
+  if (count < 0 || first < 0 || n < 0 || first + n > count) return fail(HB_ERR_CONFIG, "bad triple range");
+  return cuda_status(hb_dealer_launch(state_lo, state_hi, inc_lo, inc_hi, kind, width, (unsigned long long)count,
+                                      (unsigned long long)first, (unsigned long long)n, a0, b0, c0, a1, b1, c1,
+                                      S(stream)),
+                     "hb_deal_triples");
+}
+
+int hb_avgpool_nhwc(const uint64_t* x, int64_t batch, int height, int width, int channels, int kh, int kw, int stride,
+                    uint64_t inv, int party, int frac_bits, uint64_t* out, void* stream) {
+  if (kh <= 0 || kw <= 0 || stride <= 0 || kh > height || kw > width || channels <= 0)
+    return fail(HB_ERR_CONFIG, "bad pool geometry");
+  return cuda_status(hb_ring_avgpool_nhwc(x, batch, height, width, channels, kh, kw, stride, inv, party, frac_bits, out,
+                                          S(stream)),
+                     "hb_avgpool_nhwc");
 }
 
 int hb_add_shares(const uint64_t* a, const uint64_t* b, int64_t n, uint64_t* out, void* stream) {

@@ -92,6 +92,24 @@ __global__ void k_avgpool(const u64* __restrict__ x, long long BC, int H, int Wd
   out[idx] = party == 0 ? (s >> frac) : (0ull - ((0ull - s) >> frac));
 }
 
+// NHWC variant: x [B, H, W, C] -> out [B, OH, OW, C]
+__global__ void k_avgpool_nhwc(const u64* __restrict__ x, long long Bn, int H, int Wd, int C, int kh, int kw,
+                               int stride, int OH, int OW, u64 inv, int party, int frac, u64* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Bn * OH * OW * C) return;
+  const int c = (int)(idx % C);
+  const long long pix = idx / C;
+  const int ow = (int)(pix % OW);
+  const long long t = pix / OW;
+  const int oh = (int)(t % OH);
+  const long long b = t / OH;
+  u64 s = 0;
+  for (int i = 0; i < kh; ++i)
+    for (int j = 0; j < kw; ++j) s += x[((b * H + oh * stride + i) * (long long)Wd + ow * stride + j) * C + c];
+  s *= inv;
+  out[idx] = party == 0 ? (s >> frac) : (0ull - ((0ull - s) >> frac));
+}
+
 // out = share + other share (mod 2^64): the residual add of ResNet blocks (sharing.py:118-122)
 __global__ void k_add(const u64* __restrict__ a, const u64* __restrict__ b, long long n, u64* __restrict__ out) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -123,6 +141,14 @@ cudaError_t hb_ring_avgpool(const hb::u64* x, long long BC, int H, int W, int kh
   const int OH = (H - kh) / stride + 1, OW = (W - kw) / stride + 1;
   if (BC * OH * OW)
     hb::k_avgpool<<<hb::nblk(BC * OH * OW), 256, 0, s>>>(x, BC, H, W, kh, kw, stride, OH, OW, inv, party, frac, out);
+  return cudaGetLastError();
+}
+
+cudaError_t hb_ring_avgpool_nhwc(const hb::u64* x, long long B, int H, int W, int C, int kh, int kw, int stride,
+                                 hb::u64 inv, int party, int frac, hb::u64* out, cudaStream_t s) {
+  const int OH = (H - kh) / stride + 1, OW = (W - kw) / stride + 1;
+  const long long n = B * OH * OW * C;
+  if (n) hb::k_avgpool_nhwc<<<hb::nblk(n), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, OH, OW, inv, party, frac, out);
   return cudaGetLastError();
 }
 

@@ -135,11 +135,38 @@ def deal_on_device(kind: str, width: int, count: int, seed: int, device=None):
     return (a ^ ra, b ^ rb, c ^ rc), (ra, rb, rc)
 
 
-def stock_on_device(stores, parties, kind: str, width: int, count: int, seed: int, chunk: int = 1 << 25) -> None:
+def pcg64_seed_state(seed: int) -> tuple:
+    """(state, inc) of default_rng(SeedSequence(seed)) before any draw -- the stream the
+    reference dealer reads (dealer.py:50-51)."""
+    st = np.random.default_rng(np.random.SeedSequence(seed)).bit_generator.state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+def deal_exact_on_device(kind: str, width: int, count: int, seed: int, first: int = 0, n: int | None = None,
+                         device=None):
+    """Triples [first, first + n) of gen_arith_triples / gen_bool_triples(count, width, seed),
+    computed in HBM by hb_deal_triples (PCG64 jump-ahead) -- bit-identical to the host
+    generator.  Returns ((a0, b0, c0), (a1, b1, c1)) CUDA int64 tensors."""
+    if count < 0:
+        raise ConfigError("count must be >= 0")
+    n = count - first if n is None else n
+    dev = device or _dev.device()
+    s, inc = pcg64_seed_state(seed)
+    out = [torch.empty(max(n, 1), dtype=torch.int64, device=dev) for _ in range(6)]
+    m64 = (1 << 64) - 1
+    _lib.call("hb_deal_triples", s & m64, s >> 64, inc & m64, inc >> 64, _CODES[kind], width, count, first, n,
+              *(t.data_ptr() for t in out), _dev.stream_handle())
+    out = [t[:n] for t in out]
+    return (out[0], out[1], out[2]), (out[3], out[4], out[5])
+
+
+def stock_on_device(stores, parties, kind: str, width: int, count: int, seed: int, chunk: int = 1 << 25,
+                    exact: bool = True) -> None:
     """Stock `count` triples of one (kind, width) into each store (store i holds party
-    parties[i]'s share), generated chunk by chunk in HBM with deal_on_device and packed
-    straight into the final stream -- peak scratch is one chunk, not the whole stock.
-    Ranks that each hold one party call this with the same seed and get matching shares."""
+    parties[i]'s share), generated chunk by chunk in HBM and packed straight into the final
+    stream -- peak scratch is one chunk, not the whole stock.  exact=True deals exactly
+    gen_*_triples(count, width, seed) (the reference dealer's stream); exact=False uses
+    torch's generator.  Ranks that each hold one party call this with the same seed."""
     dev = _dev.device()
     chunk = max(64, (chunk // 64) * 64)  # whole 64-bit words per chunk for any width
     if kind == BOOL:
@@ -149,7 +176,8 @@ def stock_on_device(stores, parties, kind: str, width: int, count: int, seed: in
         outs = [[torch.empty(max(count, 1), dtype=torch.int64, device=dev) for _ in range(3)] for _ in stores]
     for i, lo in enumerate(range(0, count, chunk)):
         c = min(chunk, count - lo)
-        shares = deal_on_device(kind, width, c, seed * 100003 + i, dev)
+        shares = (deal_exact_on_device(kind, width, count, seed, lo, c, dev) if exact
+                  else deal_on_device(kind, width, c, seed * 100003 + i, dev))
         for out, p in zip(outs, parties):
             for dst, src in zip(out, shares[p]):
                 if kind == BOOL:

@@ -242,8 +242,13 @@ def _balanced_limbs(w: np.ndarray):
 
 
 def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) -> _LimbWeight:
-    w_enc = ring.to_signed(ring.encode_array(np.asarray(weight, dtype=np.float64), cfg), 64)
-    n, k = w_enc.shape
+    """Encode W once, split it into balanced byte limbs, lay the limbs out for both GEMM paths:
+    bt (cuBLASLt, NCHW patch order c*kh*kw + ki*kw + kj) and wl_tc (tcgen05 kernel, NHWC patch
+    order (ki*kw + kj)*C + c, UMMA tiles)."""
+    w = np.asarray(weight)
+    n = w.shape[0]
+    w_enc = ring.to_signed(ring.encode_array(w.reshape(n, -1).astype(np.float64), cfg), 64)
+    k = w_enc.shape[1]
     kp, np_ = -(-k // 16) * 16, -(-n // 8) * 8
     limbs = _balanced_limbs(w_enc)
     j = len(limbs)
@@ -257,9 +262,10 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
     lw = _LimbWeight(n, k, kp, np_, j, torch.from_numpy(bt.reshape(j * np_, kp)).to(dev),
                      torch.from_numpy(colsum).to(dev), torch.from_numpy(b.view(np.int64)).to(dev))
     if j <= 3 and k <= 21900:
+        nhwc = [l.reshape(w.shape).transpose(0, 2, 3, 1).reshape(n, k) if w.ndim == 4 else l for l in limbs]
         lw.nt = 64 if n >= 64 else (32 if n > 16 else 16)
         lw.kp_tc = -(-k // 64) * 64
-        lw.wl_tc = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt, lw.kp_tc)).to(dev)
+        lw.wl_tc = torch.from_numpy(_tc_tiles(nhwc, n, k, lw.nt, lw.kp_tc)).to(dev)
     return lw
 
 
@@ -283,7 +289,7 @@ def _weight(weight, bias, cfg) -> _LimbWeight:
     key = (id(weight), id(bias), cfg)
     hit = _WCACHE.get(key)
     if hit is None or hit[0] is not weight or hit[1] is not bias:
-        hit = (weight, bias, _prep_weight(np.asarray(weight).reshape(weight.shape[0], -1), bias, cfg))
+        hit = (weight, bias, _prep_weight(weight, bias, cfg))
         _WCACHE[key] = hit
     return hit[2]
 
@@ -291,26 +297,79 @@ def _weight(weight, bias, cfg) -> _LimbWeight:
 RING_GEMM = os.environ.get("HB_RING_GEMM", "tc")  # "tc" (hand-written tcgen05) or "cublaslt"
 
 
-def _ring_gemm(xd: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int, layout: int, spatial: int):
-    """One party's (patches(x) @ W^T) mod 2^64 -> truncate -> + bias, on the GPU."""
-    b, c, h, w, kh, kw, stride, pad = geom
+def _use_tc(lw: _LimbWeight) -> bool:
+    return RING_GEMM == "tc" and lw.wl_tc is not None
+
+
+def _gemm_tc(x_nhwc: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int) -> torch.Tensor:
+    """Fused tcgen05 kernel: NHWC share in, NHWC [b, oh, ow, n] share out."""
+    b, h, w, c = x_nhwc.shape
+    kh, kw, stride, pad = geom
+    oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    out = torch.empty((b, oh, ow, lw.n), dtype=torch.int64, device=x_nhwc.device)
+    _lib.call("hb_conv_limbs_tc", x_nhwc.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
+              lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(),
+              _dev.stream_handle())
+    return out
+
+
+def _gemm_cublaslt(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int, layout: int) -> torch.Tensor:
+    """im2col + limb split kernel, one cuBLASLt int8 GEMM over all limb pairs, combine kernel.
+    layout 1: NCHW [b, n, oh, ow] out (conv); 0: [b, n] (linear)."""
+    b, c, h, w = x_nchw.shape
+    kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
     m = b * oh * ow
     s = _dev.stream_handle()
-    if RING_GEMM == "tc" and lw.wl_tc is not None:
-        # fused tcgen05 kernel: output is NCHW, which for linear (1x1 spatial) is [b, n]
-        out = torch.empty(m * lw.n, dtype=torch.int64, device=xd.device)
-        _lib.call("hb_conv_limbs_tc", xd.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n,
-                  lw.j, lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
-        return out
-    a = torch.empty((8 * m, lw.kp), dtype=torch.int8, device=xd.device)
-    _lib.call("hb_im2col_limbs", xd.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.kp, a.data_ptr(), s)
+    a = torch.empty((8 * m, lw.kp), dtype=torch.int8, device=x_nchw.device)
+    _lib.call("hb_im2col_limbs", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.kp, a.data_ptr(), s)
     if 8 * m <= 16:  # the int8 GEMM needs more than 16 rows; padded rows are ignored
         a = torch.cat([a, torch.zeros((24 - 8 * m, lw.kp), dtype=torch.int8, device=a.device)])
     prod = torch._int_mm(a, lw.bt.t())  # [8m(+pad), J*Np] int32 -- tensor cores
-    out = torch.empty(m * lw.n, dtype=torch.int64, device=xd.device)
+    out = torch.empty(m * lw.n, dtype=torch.int64, device=x_nchw.device)
     _lib.call("hb_limb_combine", prod.data_ptr(), m, lw.n, lw.np_, lw.j, lw.colsum.data_ptr(), party, frac,
-              lw.bias.data_ptr() if party == 0 else None, layout, spatial, out.data_ptr(), s)
+              lw.bias.data_ptr() if party == 0 else None, layout, oh * ow, out.data_ptr(), s)
+    return out.view(b, lw.n, oh, ow) if layout == 1 else out.view(b, lw.n)
+
+
+def _to_layout(d: torch.Tensor, have: str, want: str) -> torch.Tensor:
+    if have == want or d.dim() != 4:
+        return d
+    if want == "nhwc":
+        return d.permute(0, 2, 3, 1).contiguous()
+    return d.permute(0, 3, 1, 2).contiguous()
+
+
+def _conv_dev(d, lay, L: Conv2d, lw, party, frac):
+    """Conv on a device share in layout `lay`; returns (output, its layout)."""
+    geom = (L.kh, L.kw, L.stride, L.pad)
+    if _use_tc(lw):
+        return _gemm_tc(_to_layout(d, lay, "nhwc"), geom, lw, party, frac), "nhwc"
+    return _gemm_cublaslt(_to_layout(d, lay, "nchw"), geom, lw, party, frac, 1), "nchw"
+
+
+def _linear_dev(d, lw, party, frac):
+    b, k = d.shape
+    if _use_tc(lw):
+        return _gemm_tc(d.reshape(b, 1, 1, k), (1, 1, 1, 0), lw, party, frac).view(b, lw.n)
+    return _gemm_cublaslt(d.reshape(b, k, 1, 1), (1, 1, 1, 0), lw, party, frac, 0)
+
+
+def _avgpool_dev(d, lay, L: AvgPool, party, cfg):
+    inv = ring.encode_fixed(1.0 / (L.kh * L.kw), cfg).value
+    s = _dev.stream_handle()
+    if lay == "nhwc":
+        b, h, w, c = d.shape
+        oh, ow = (h - L.kh) // L.stride + 1, (w - L.kw) // L.stride + 1
+        out = torch.empty((b, oh, ow, c), dtype=torch.int64, device=d.device)
+        _lib.call("hb_avgpool_nhwc", d.data_ptr(), b, h, w, c, L.kh, L.kw, L.stride, inv, party, cfg.frac_bits,
+                  out.data_ptr(), s)
+        return out
+    b, c, h, w = d.shape
+    oh, ow = (h - L.kh) // L.stride + 1, (w - L.kw) // L.stride + 1
+    out = torch.empty((b, c, oh, ow), dtype=torch.int64, device=d.device)
+    _lib.call("hb_avgpool", d.data_ptr(), b * c, h, w, L.kh, L.kw, L.stride, inv, party, cfg.frac_bits,
+              out.data_ptr(), s)
     return out
 
 
@@ -336,26 +395,19 @@ def linear_forward(session: ProtocolSession, x: ArithShareTensor, weight, bias) 
     _check_ring(x, cfg)
     if len(x.shape) != 2 or x.shape[1] != weight.shape[1]:
         raise ConfigError(f"linear expects [batch, {weight.shape[1]}], got {x.shape}")
-    lw = _weight(weight, bias, cfg)
-    xd = _dev.to_device(x.data)
-    b, k = x.shape
-    out = _ring_gemm(xd, (b, k, 1, 1, 1, 1, 1, 0), lw, x.party, cfg.frac_bits, 0, 1)
-    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, lw.n), x.data))
+    out = _linear_dev(_dev.to_device(x.data), _weight(weight, bias, cfg), x.party, cfg.frac_bits)
+    return ArithShareTensor(x.party, 64, _dev.to_host(out, x.data))
 
 
 def conv2d_forward(session: ProtocolSession, x: ArithShareTensor, layer: Conv2d, weight, bias) -> ArithShareTensor:
-    """Convolution as fused im2col + ring GEMM (nn.py:227-243)."""
+    """Convolution on NCHW shares (nn.py:227-243): fused tcgen05 kernel (NHWC inside) or
+    im2col + cuBLASLt limb GEMM."""
     cfg = session.fxp
     _check_ring(x, cfg)
     if len(x.shape) != 4 or x.shape[1] != layer.in_channels:
         raise ConfigError(f"conv expects [batch, {layer.in_channels}, H, W], got {x.shape}")
-    lw = _weight(weight, bias, cfg)
-    xd = _dev.to_device(x.data)
-    b, c, h, w = x.shape
-    oh, ow = (h + 2 * layer.pad - layer.kh) // layer.stride + 1, (w + 2 * layer.pad - layer.kw) // layer.stride + 1
-    out = _ring_gemm(xd, (b, c, h, w, layer.kh, layer.kw, layer.stride, layer.pad), lw, x.party, cfg.frac_bits, 1,
-                     oh * ow)
-    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, layer.out_channels, oh, ow), x.data))
+    out, lay = _conv_dev(_dev.to_device(x.data), "nchw", layer, _weight(weight, bias, cfg), x.party, cfg.frac_bits)
+    return ArithShareTensor(x.party, 64, _dev.to_host(_to_layout(out, lay, "nchw"), x.data))
 
 
 def avgpool_forward(session: ProtocolSession, x: ArithShareTensor, layer: AvgPool) -> ArithShareTensor:
@@ -364,14 +416,8 @@ def avgpool_forward(session: ProtocolSession, x: ArithShareTensor, layer: AvgPoo
     _check_ring(x, cfg)
     if len(x.shape) != 4:
         raise ConfigError(f"avgpool expects [batch, C, H, W], got {x.shape}")
-    b, c, h, w = x.shape
-    oh, ow = (h - layer.kh) // layer.stride + 1, (w - layer.kw) // layer.stride + 1
-    inv = ring.encode_fixed(1.0 / (layer.kh * layer.kw), cfg).value
-    xd = _dev.to_device(x.data)
-    out = torch.empty(b * c * oh * ow, dtype=torch.int64, device=xd.device)
-    _lib.call("hb_avgpool", xd.data_ptr(), b * c, h, w, layer.kh, layer.kw, layer.stride, inv, x.party,
-              cfg.frac_bits, out.data_ptr(), _dev.stream_handle())
-    return ArithShareTensor(x.party, 64, _dev.to_host(out.reshape(b, c, oh, ow), x.data))
+    out = _avgpool_dev(_dev.to_device(x.data), "nchw", layer, x.party, cfg)
+    return ArithShareTensor(x.party, 64, _dev.to_host(out, x.data))
 
 
 def relu_forward(session: ProtocolSession, x: ArithShareTensor, window) -> ArithShareTensor:
@@ -379,23 +425,11 @@ def relu_forward(session: ProtocolSession, x: ArithShareTensor, window) -> Arith
     return x if window is None else protocol.relu(session, x, window)
 
 
-def _add(a: ArithShareTensor, b: ArithShareTensor) -> ArithShareTensor:
-    ad, bd = _dev.to_device(a.data), _dev.to_device(b.data)
-    out = torch.empty_like(ad)
-    _lib.call("hb_add_shares", ad.data_ptr(), bd.data_ptr(), ad.numel(), out.data_ptr(), _dev.stream_handle())
-    return ArithShareTensor(a.party, a.width, _dev.to_host(out, a.data))
-
-
-def _local_layer(session, cur, L, model):
-    if isinstance(L, Linear):
-        return linear_forward(session, cur, model.weights[L.weight], model.weights[L.bias])
-    if isinstance(L, Conv2d):
-        return conv2d_forward(session, cur, L, model.weights[L.weight], model.weights[L.bias])
-    if isinstance(L, AvgPool):
-        return avgpool_forward(session, cur, L)
-    if isinstance(L, Flatten):
-        return ArithShareTensor(cur.party, cur.width, cur.data.reshape(cur.shape[0], -1))
-    raise ConfigError(f"unknown layer kind {L!r}")
+def _add_dev(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(a)
+    _lib.call("hb_add_shares", a.data_ptr(), b.contiguous().data_ptr(), a.numel(), out.data_ptr(),
+              _dev.stream_handle())
+    return out
 
 
 def _meter_delta(ep, before):
@@ -403,64 +437,73 @@ def _meter_delta(ep, before):
     return sum(after[t][0] - before[t][0] for t in after), sum(after[t][1] - before[t][1] for t in after)
 
 
+def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_meter):
+    """Run the layers for one party (model_forward) or both parties on this GPU
+    (model_forward_pair).  Shares stay on the device; conv activations stay NHWC
+    between layers (tcgen05 path), NCHW is restored only where order matters
+    (Flatten of a spatial map, the caller's output)."""
+    if len(relu_cfg.windows) != model.n_groups:
+        raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
+    cfg = model.fixed_point
+    parties = [s.party for s in sessions]
+
+    def run(layers, ds, lay, prefix):
+        for i, L in enumerate(layers):
+            before = [s.endpoint.meter.snapshot() for s in sessions]
+            if isinstance(L, Relu):
+                win = relu_cfg.window_for(L.group_id)
+                if win is not None:
+                    shares = [ArithShareTensor(p, 64, d) for p, d in zip(parties, ds)]
+                    if len(sessions) == 2:
+                        out = protocol.relu_pair(tuple(sessions), shares[0], shares[1], win)
+                    else:
+                        out = [protocol.relu(sessions[0], shares[0], win)]
+                    ds = [o.data for o in out]
+            elif isinstance(L, Residual):
+                a, la = run(L.body, ds, lay, f"{prefix}{i}.body.")
+                h, lh = run(L.shortcut, ds, lay, f"{prefix}{i}.short.")
+                ds = [_add_dev(x, _to_layout(y, lh, la)) for x, y in zip(a, h)]
+                lay = la
+            elif isinstance(L, Conv2d):
+                lw = _weight(model.weights[L.weight], model.weights[L.bias], cfg)
+                res = [_conv_dev(d, lay, L, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]
+                ds, lay = [r[0] for r in res], res[0][1]
+            elif isinstance(L, Linear):
+                lw = _weight(model.weights[L.weight], model.weights[L.bias], cfg)
+                ds = [_linear_dev(d, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]
+            elif isinstance(L, AvgPool):
+                ds = [_avgpool_dev(d, lay, L, p, cfg) for d, p in zip(ds, parties)]
+            elif isinstance(L, Flatten):
+                ds = [_to_layout(d, lay, "nchw").reshape(d.shape[0], -1) for d in ds]
+                lay = "flat"
+            else:
+                raise ConfigError(f"unknown layer kind {L!r}")
+            if layer_meter is not None:
+                for p, (s, bef) in enumerate(zip(sessions, before)):
+                    nb, nr = _meter_delta(s.endpoint, bef)
+                    layer_meter[p].append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
+        return ds, lay
+
+    ds, lay = run(model.layers, datas, "nchw" if datas[0].dim() == 4 else "flat", "")
+    return [_to_layout(d, lay, "nchw") for d in ds]
+
+
 def model_forward(session: ProtocolSession, x: ArithShareTensor, model: ModelSpec, relu_cfg: ReluConfig,
                   layer_meter: list | None = None) -> ArithShareTensor:
     """One party runs every layer (nn.py:271-307); shares stay on the GPU between layers."""
-    if len(relu_cfg.windows) != model.n_groups:
-        raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
-
-    def run(layers, cur, prefix):
-        for i, L in enumerate(layers):
-            before = session.endpoint.meter.snapshot()
-            if isinstance(L, Relu):
-                cur = relu_forward(session, cur, relu_cfg.window_for(L.group_id))
-            elif isinstance(L, Residual):
-                cur = _add(run(L.body, cur, f"{prefix}{i}.body."), run(L.shortcut, cur, f"{prefix}{i}.short."))
-            else:
-                cur = _local_layer(session, cur, L, model)
-            if layer_meter is not None:
-                nb, nr = _meter_delta(session.endpoint, before)
-                layer_meter.append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
-        return cur
-
-    host_in = x.data
-    cur = ArithShareTensor(x.party, x.width, _dev.to_device(x.data))
-    out = run(model.layers, cur, "")
-    return ArithShareTensor(out.party, out.width, _dev.to_host(out.data, host_in))
+    (out,) = _run_model([session], [_dev.to_device(x.data)], model, relu_cfg,
+                        None if layer_meter is None else (layer_meter,))
+    return ArithShareTensor(x.party, x.width, _dev.to_host(out, x.data))
 
 
 def model_forward_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, model: ModelSpec,
                        relu_cfg: ReluConfig, layer_meter: tuple | None = None):
     """Both parties on this GPU: local layers per party, every ReLU through the fused
     pair kernel (protocol.relu_pair).  Same shares and meters as two model_forward threads."""
-    if len(relu_cfg.windows) != model.n_groups:
-        raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
-    s0, s1 = sessions
-
-    def run(layers, c0, c1, prefix):
-        for i, L in enumerate(layers):
-            b0, b1 = s0.endpoint.meter.snapshot(), s1.endpoint.meter.snapshot()
-            if isinstance(L, Relu):
-                win = relu_cfg.window_for(L.group_id)
-                if win is not None:
-                    c0, c1 = protocol.relu_pair((s0, s1), c0, c1, win)
-            elif isinstance(L, Residual):
-                a0, a1 = run(L.body, c0, c1, f"{prefix}{i}.body.")
-                h0, h1 = run(L.shortcut, c0, c1, f"{prefix}{i}.short.")
-                c0, c1 = _add(a0, h0), _add(a1, h1)
-            else:
-                c0, c1 = _local_layer(s0, c0, L, model), _local_layer(s1, c1, L, model)
-            if layer_meter is not None:
-                for p, (s, bef) in enumerate(((s0, b0), (s1, b1))):
-                    nb, nr = _meter_delta(s.endpoint, bef)
-                    layer_meter[p].append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
-        return c0, c1
-
-    d0 = ArithShareTensor(0, x0.width, _dev.to_device(x0.data))
-    d1 = ArithShareTensor(1, x1.width, _dev.to_device(x1.data))
-    o0, o1 = run(model.layers, d0, d1, "")
-    return (ArithShareTensor(0, o0.width, _dev.to_host(o0.data, x0.data)),
-            ArithShareTensor(1, o1.width, _dev.to_host(o1.data, x1.data)))
+    o0, o1 = _run_model(list(sessions), [_dev.to_device(x0.data), _dev.to_device(x1.data)], model, relu_cfg,
+                        layer_meter)
+    return (ArithShareTensor(0, x0.width, _dev.to_host(o0, x0.data)),
+            ArithShareTensor(1, x1.width, _dev.to_host(o1, x1.data)))
 
 
 def triple_requirements(model: ModelSpec, relu_cfg: ReluConfig, batch: int) -> dict:

@@ -259,3 +259,44 @@ def test_theorem1_exhaustive_gpu():
     for k in range(2, 8):
         inr = (signed >= -(2 ** (k - 1))) & (signed < 2 ** (k - 1))
         assert np.array_equal(run(k)[inr], full[inr])
+
+
+# ------------------------------------------------------------------ on-device dealer
+@pytest.mark.parametrize("kind,count,width,seed", [("arith", 1000, 16, 1234), ("arith", 777, 64, 9),
+                                                    ("bool", 1000, 8, 3), ("bool", 513, 6, 11), ("arith", 100, 10, 5),
+                                                    ("bool", 70001, 13, 77)])
+def test_device_dealer_bit_exact(kind, count, width, seed):
+    from paper_2309_04875_b200 import dealer
+
+    host = (dealer.gen_arith_triples if kind == "arith" else dealer.gen_bool_triples)(count, width, seed)
+    dev = dealer.deal_exact_on_device(kind, width, count, seed)
+    for p in (0, 1):
+        for h, d in zip(host.party_arrays(p), dev[p]):
+            assert np.array_equal(h, d.cpu().numpy().view(np.uint64))
+    # a sub-range equals the same slice of the full batch (chunked stocking)
+    part = dealer.deal_exact_on_device(kind, width, count, seed, first=count // 3, n=count // 2)
+    assert np.array_equal(part[0][0].cpu().numpy().view(np.uint64), host.party_arrays(0)[0][count // 3:count // 3 + count // 2])
+
+
+def test_device_dealer_golden_file_sha(tmp_path, golden):
+    from paper_2309_04875_b200 import dealer
+
+    dev = dealer.deal_exact_on_device("arith", 16, 1000, 1234)
+    batch = dealer.TripleBatch("arith", 16, 1000, 1234,
+                               tuple(tuple(t.cpu().numpy().view(np.uint64) for t in dev[p]) for p in (0, 1)))
+    dealer.save_triples(batch, tmp_path / "g.bin")
+    import hashlib
+
+    assert hashlib.sha256((tmp_path / "g.bin").read_bytes()).hexdigest() == golden[0]["dealer_hbtrip1_sha"]["sha"]
+
+
+def test_stock_on_device_matches_reference_stream():
+    """Chunked exact stocking == gen_*_triples stocked through add_batch, stream for stream."""
+    from paper_2309_04875_b200 import dealer
+
+    a, b = dealer.TripleStore(0), dealer.TripleStore(0)
+    dealer.stock_on_device((a,), (0,), "bool", 8, 10_000, 5, chunk=1024)
+    b.add_batch(dealer.gen_bool_triples(10_000, 8, 5))
+    va, vb = a.draw("bool", 8, 10_000), b.draw("bool", 8, 10_000)
+    for x, y in zip(va.unpacked(), vb.unpacked()):
+        assert np.array_equal(x, y)
