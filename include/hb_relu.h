@@ -73,6 +73,12 @@ int hb_relu_pair(int ring_bits, int k, int m, int64_t n,
                  const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
                  hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
                  int drelu_only, void* stream);
+/* Same, for the elements [first, first + count) of an n-element layer (triple segments still
+ * n apart): lets a host pipeline H2D / compute / D2H chunks of one layer across streams. */
+int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, int64_t count,
+                       const uint64_t* x0, const uint64_t* x1, uint64_t* y0, uint64_t* y1,
+                       hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                       int drelu_only, void* stream);
 
 /* ---- one party, staged: protocol.relu / protocol.drelu (protocol.py:179-199)
  * split at its exchanges.  Call round r = 0 .. hb_relu_rounds(): round r writes
@@ -162,11 +168,10 @@ int hb_deal_triples(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint6
 
 /* Fused ring conv/linear on tcgen05 tensor cores (hand-written, sm_100a): im2col gather, byte-limb
  * split, u8 x s8 -> s32 MMAs with the 8 byte-shift accumulators in TMEM, fold mod 2^64, local
- * truncation, party-0 bias -- one kernel, no int32 intermediates in HBM.
- * Layouts are NHWC: x [batch][height][width][channels], y [batch][OH][OW][n_out] (a linear layer is
- * the 1x1 case, x [batch][K]); patch index k = (ki*kw + kj)*channels + c.
- * wlimbs: int8 [ceil(n_out/n_tile)][k_padded/64][j_limbs][n_tile x 64 UMMA canonical K-major tile],
- * built from the weight permuted to [n_out][kh][kw][channels];
+ * truncation, party-0 bias, NCHW store -- one kernel, no int32 intermediates in HBM.
+ * x NCHW [batch][channels][height][width] (a linear layer is the 1x1 case [batch][K]), y NCHW
+ * [batch][n_out][OH][OW]; patch index k = c*kh*kw + ki*kw + kj (nn.py:177-195).
+ * wlimbs: int8 [ceil(n_out/n_tile)][k_padded/64][j_limbs][n_tile x 64 UMMA canonical K-major tile];
  * k_padded % 64 == 0, C*kh*kw <= 21900, j_limbs <= 3, n_tile in {16, 32, 64}. */
 int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
                      int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,

@@ -57,6 +57,9 @@ _SIGS = {
     "hb_relu_round_tag": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hb_relu_pair": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p, u64p, u64p,
                                     Triples, Triples, Triples, Triples, ctypes.c_int, ctypes.c_void_p]),
+    "hb_relu_pair_range": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, u64p, u64p, u64p, u64p, Triples, Triples, Triples, Triples,
+                                          ctypes.c_int, ctypes.c_void_p]),
     "hb_relu_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "hb_relu_round": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                      ctypes.c_int, u64p, u64p, Triples, Triples, ctypes.c_void_p, u64p, u64p,

@@ -200,6 +200,14 @@ int hb_relu_round_tag(int k, int m, int round) {
 int hb_relu_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
                  uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
                  int drelu_only, void* stream) {
+  return hb_relu_pair_range(ring_bits, k, m, n, 0, n, x0, x1, y0, y1, bool0, bool1, arith0, arith1, drelu_only,
+                            stream);
+}
+
+int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, int64_t count, const uint64_t* x0,
+                       const uint64_t* x1, uint64_t* y0, uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1,
+                       hb_triples_t arith0, hb_triples_t arith1, int drelu_only, void* stream) {
+  if (first < 0 || count < 0 || first + count > n) return fail(HB_ERR_CONFIG, "element range outside the layer");
   int rc = check_window(ring_bits, k, m);
   if (rc) return rc;
   if (n < 0) return fail(HB_ERR_CONFIG, "negative element count");
@@ -208,11 +216,13 @@ int hb_relu_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, con
   if ((rc = check_triples(bool0, "bool", w, nb, 0)) || (rc = check_triples(bool1, "bool", w, nb, 1)) ||
       (rc = check_triples(arith0, "arith", ring_bits, na, 0)) || (rc = check_triples(arith1, "arith", ring_bits, na, 1)))
     return rc;
-  if (n == 0) return HB_OK;
+  if (count == 0) return HB_OK;
   hb::PairArgs A;
   A.io[0] = make_io(x0, y0, bool0, arith0, w);
   A.io[1] = make_io(x1, y1, bool1, arith1, w);
   A.n = (u64)n;
+  A.first = (u64)first;
+  A.count = (u64)count;
   A.N = ring_bits;
   A.m = m;
   A.drelu_only = drelu_only ? 1 : 0;

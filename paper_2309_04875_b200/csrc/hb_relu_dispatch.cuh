@@ -19,7 +19,7 @@ size_t pair_smem_bytes() {
 template <int W, bool R64>
 cudaError_t launch_pair_impl(const PairArgs& A, cudaStream_t s) {
   constexpr int GS = Geo<W>::GS;
-  const u64 ngroups = (A.n + GS - 1) / GS;
+  const u64 ngroups = (A.count + GS - 1) / GS;
   const u64 blocks = (ngroups + PAIR_TP - 1) / PAIR_TP;
   const size_t smem = pair_smem_bytes<W>();
   static bool configured = false;  // benign race: idempotent attribute set

@@ -47,9 +47,11 @@ struct PartyIO {
 
 struct PairArgs {
   PartyIO io[2];
-  u64 n;
-  int N;  // ring bits
-  int m;  // window low bit
+  u64 n;      // layer size: stride between the triple segments
+  u64 first;  // this launch covers elements [first, first + count)
+  u64 count;
+  int N;      // ring bits
+  int m;      // window low bit
   int drelu_only;
 };
 
@@ -135,8 +137,9 @@ __global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairAr
   const int t = threadIdx.x - party * TP;
   const bool p0 = party == 0;
   const u64 n = A.n;
-  const u64 e0 = ((u64)blockIdx.x * TP + t) * GS;
-  const int valid = e0 >= n ? 0 : (int)min((u64)GS, n - e0);
+  const u64 end = A.first + A.count;
+  const u64 e0 = A.first + ((u64)blockIdx.x * TP + t) * GS;
+  const int valid = e0 >= end ? 0 : (int)min((u64)GS, end - e0);
   const PartyIO& io = A.io[party];
   const u64 MN = RING64 ? ~0ull : nmask(A.N);  // Z/2^64: masks fold away at compile time
   const bool mult = !A.drelu_only;

@@ -11,20 +11,16 @@
 // so nothing but x, the weight limbs and y ever touches HBM (the cuBLASLt path
 // writes 8*J int32 partial products per output).
 //
-// Activations are NHWC and the patch index is k = (ki*kw + kj)*C + c, so for C a
-// multiple of 16 every 16-value K chunk of a patch row is 128 contiguous bytes of x.
-//
-// CTA: 512 threads, output tile 128 rows (M = batch*OH*OW) x N_T columns.
-//   mainloop, per K block of 64: 4 threads per row each gather one 16-value chunk
-//   (all loads issued first), split it into 8 limb planes with 4x4 byte transposes
-//   and store them in shared memory in the UMMA canonical K-major no-swizzle layout
-//   (8x16B core matrices); the weight-limb tile is copied as-is (host pre-lays it
-//   out).  One elected thread issues the MMAs and tcgen05.commit's a per-stage
-//   mbarrier; two stages, so the gather of block k+1 overlaps the tensor-core work
-//   of block k.
-//   epilogue: warp w reads TMEM lane quarter w%4 for column group w/4, folds the 8
-//   shifts mod 2^64, truncates (party-dependent), adds the party-0 bias and stores
-//   the [M, N] = NHWC output row.
+// CTA: 128 threads, output tile 128 rows (M = batch*OH*OW) x N_T columns.
+//   mainloop, per K block of 64:  all threads gather the im2col patch values of
+//   the tile (u64), split them into 8 limb planes and store them in shared memory
+//   in the UMMA canonical K-major no-swizzle layout (8x16B core matrices); the
+//   weight-limb tile is copied as-is (host pre-lays it out).  One elected thread
+//   issues the MMAs and tcgen05.commit's a per-stage mbarrier; two stages, so the
+//   gather of block k+1 overlaps the tensor-core work of block k.
+//   epilogue: each thread owns one accumulator row (TMEM lane), tcgen05.ld's its
+//   8 x N_T values, folds the shifts mod 2^64, truncates (party-dependent), adds
+//   the party-0 bias and stores NCHW (consecutive threads = consecutive pixels).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -160,43 +156,33 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
     oh = rem / A.OW;
     ow = rem - oh * A.OW;
   }
+  const int khw = A.kh * A.kw;
   const int ih0 = oh * A.stride - A.pad, iw0 = ow * A.stride - A.pad;
-  const u64* xb = A.x + (long long)b * A.H * A.W * A.C;
-  const bool vec = (A.C & 15) == 0;  // 16-value chunks never straddle a (ki, kj) tap
+  const long long HW = (long long)A.H * A.W;
+  const u64* xb = A.x + (long long)b * A.C * HW;
 
   uint32_t phase[2] = {0, 0};
   for (int kb = 0; kb < nkb; ++kb) {
     const int st = kb & 1;
     uint8_t* sA = smem + st * stage_bytes;
     uint8_t* sB = sA + 8 * PLANE;
-    // ---- gather 16 patch values (all loads issued before any use); k = (ki*kw + kj)*C + c
+    // ---- gather 16 patch values (all loads issued before any use); k = c*khw + ki*kw + kj
     u64 v[16];
     {
       const int k0 = kb * KB + q * 16;
-      if (vec) {
-        const int t = k0 / A.C, c0 = k0 - t * A.C;
-        const int ki = t / A.kw, kj = t - ki * A.kw;
+      int c = k0 / khw;
+      const int t0 = k0 - c * khw;
+      int ki = t0 / A.kw, kj = t0 - ki * A.kw;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
         const int ih = ih0 + ki, iw = iw0 + kj;
-        const bool ok = row_ok && k0 < A.K && (unsigned)ih < (unsigned)A.H && (unsigned)iw < (unsigned)A.W;
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(xb + ((long long)ih * A.W + iw) * A.C + c0);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const ulonglong2 p2 = ok ? __ldg(src + e) : make_ulonglong2(0ull, 0ull);
-          v[2 * e] = p2.x;
-          v[2 * e + 1] = p2.y;
-        }
-      } else {
-        int t = k0 / A.C, c = k0 - t * A.C;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int ki = t / A.kw, kj = t - ki * A.kw;
-          const int ih = ih0 + ki, iw = iw0 + kj;
-          const bool ok = row_ok && (k0 + e < A.K) && (unsigned)ih < (unsigned)A.H && (unsigned)iw < (unsigned)A.W;
-          v[e] = ok ? (u64)__ldg(reinterpret_cast<const unsigned long long*>(xb + ((long long)ih * A.W + iw) * A.C + c))
-                    : 0ull;
-          if (++c == A.C) {
-            c = 0;
-            ++t;
+        const bool ok = row_ok && (k0 + e < A.K) && (unsigned)ih < (unsigned)A.H && (unsigned)iw < (unsigned)A.W;
+        v[e] = ok ? (u64)__ldg(reinterpret_cast<const unsigned long long*>(xb + c * HW + (long long)ih * A.W + iw)) : 0ull;
+        if (++kj == A.kw) {
+          kj = 0;
+          if (++ki == A.kh) {
+            ki = 0;
+            ++c;
           }
         }
       }
@@ -264,6 +250,8 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
     const int er = quarter * 32 + (tid & 31);  // this thread's accumulator row
     const long long em = m0 + er;
     const bool eok = em < A.M;
+    const int eb = eok ? (int)(em / S) : 0;
+    const long long esp = eok ? em - (long long)eb * S : 0;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
     for (int c0 = cgrp * CPG; c0 < (cgrp + 1) * CPG; c0 += 8) {
@@ -285,7 +273,7 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
           if (n < A.N) {
             u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
             if (A.party == 0 && A.bias) yv += A.bias[n];
-            A.y[em * A.N + n] = yv;  // NHWC: row m = (b, oh, ow), column n = channel
+            A.y[((long long)eb * A.N + n) * S + esp] = yv;
           }
         }
       }

@@ -243,8 +243,8 @@ def _balanced_limbs(w: np.ndarray):
 
 def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) -> _LimbWeight:
     """Encode W once, split it into balanced byte limbs, lay the limbs out for both GEMM paths:
-    bt (cuBLASLt, NCHW patch order c*kh*kw + ki*kw + kj) and wl_tc (tcgen05 kernel, NHWC patch
-    order (ki*kw + kj)*C + c, UMMA tiles)."""
+    bt (cuBLASLt) and wl_tc (tcgen05 kernel, UMMA tiles), both in the reference im2col patch
+    order c*kh*kw + ki*kw + kj (nn.py:177-195)."""
     w = np.asarray(weight)
     n = w.shape[0]
     w_enc = ring.to_signed(ring.encode_array(w.reshape(n, -1).astype(np.float64), cfg), 64)
@@ -262,10 +262,9 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
     lw = _LimbWeight(n, k, kp, np_, j, torch.from_numpy(bt.reshape(j * np_, kp)).to(dev),
                      torch.from_numpy(colsum).to(dev), torch.from_numpy(b.view(np.int64)).to(dev))
     if j <= 3 and k <= 21900:
-        nhwc = [l.reshape(w.shape).transpose(0, 2, 3, 1).reshape(n, k) if w.ndim == 4 else l for l in limbs]
         lw.nt = 64 if n >= 64 else (32 if n > 16 else 16)
         lw.kp_tc = -(-k // 64) * 64
-        lw.wl_tc = torch.from_numpy(_tc_tiles(nhwc, n, k, lw.nt, lw.kp_tc)).to(dev)
+        lw.wl_tc = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt, lw.kp_tc)).to(dev)
     return lw
 
 
@@ -301,13 +300,13 @@ def _use_tc(lw: _LimbWeight) -> bool:
     return RING_GEMM == "tc" and lw.wl_tc is not None
 
 
-def _gemm_tc(x_nhwc: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int) -> torch.Tensor:
-    """Fused tcgen05 kernel: NHWC share in, NHWC [b, oh, ow, n] share out."""
-    b, h, w, c = x_nhwc.shape
+def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int) -> torch.Tensor:
+    """Fused tcgen05 kernel (hb_conv_limbs_tc): NCHW share in, NCHW [b, n, oh, ow] share out."""
+    b, c, h, w = x_nchw.shape
     kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
-    out = torch.empty((b, oh, ow, lw.n), dtype=torch.int64, device=x_nhwc.device)
-    _lib.call("hb_conv_limbs_tc", x_nhwc.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
+    out = torch.empty((b, lw.n, oh, ow), dtype=torch.int64, device=x_nchw.device)
+    _lib.call("hb_conv_limbs_tc", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
               lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(),
               _dev.stream_handle())
     return out
@@ -343,15 +342,16 @@ def _to_layout(d: torch.Tensor, have: str, want: str) -> torch.Tensor:
 def _conv_dev(d, lay, L: Conv2d, lw, party, frac):
     """Conv on a device share in layout `lay`; returns (output, its layout)."""
     geom = (L.kh, L.kw, L.stride, L.pad)
+    d = _to_layout(d, lay, "nchw")
     if _use_tc(lw):
-        return _gemm_tc(_to_layout(d, lay, "nhwc"), geom, lw, party, frac), "nhwc"
-    return _gemm_cublaslt(_to_layout(d, lay, "nchw"), geom, lw, party, frac, 1), "nchw"
+        return _gemm_tc(d, geom, lw, party, frac), "nchw"
+    return _gemm_cublaslt(d, geom, lw, party, frac, 1), "nchw"
 
 
 def _linear_dev(d, lw, party, frac):
     b, k = d.shape
     if _use_tc(lw):
-        return _gemm_tc(d.reshape(b, 1, 1, k), (1, 1, 1, 0), lw, party, frac).view(b, lw.n)
+        return _gemm_tc(d.reshape(b, k, 1, 1), (1, 1, 1, 0), lw, party, frac).view(b, lw.n)
     return _gemm_cublaslt(d.reshape(b, k, 1, 1), (1, 1, 1, 0), lw, party, frac, 0)
 
 
@@ -439,9 +439,9 @@ def _meter_delta(ep, before):
 
 def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_meter):
     """Run the layers for one party (model_forward) or both parties on this GPU
-    (model_forward_pair).  Shares stay on the device; conv activations stay NHWC
-    between layers (tcgen05 path), NCHW is restored only where order matters
-    (Flatten of a spatial map, the caller's output)."""
+    (model_forward_pair).  Shares stay on the device between layers, in NCHW: the
+    ReLU consumes triples in element order, so keeping the reference's element order
+    is what makes the per-party shares (and the truncation after them) bit-exact."""
     if len(relu_cfg.windows) != model.n_groups:
         raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
     cfg = model.fixed_point

@@ -227,19 +227,62 @@ def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitW
         raise ConfigError("relu_pair shares must agree in width and shape")
     window.check_fits(x0.width)
     N, w = x0.width, window.width
-    a0, a1 = _flat(x0.data), _flat(x1.data)
-    n = a0.numel()
+    host_pipeline = all(isinstance(x.data, torch.Tensor) and not x.data.is_cuda and x.data.is_pinned()
+                        for x in (x0, x1)) and x0.numel > (1 << 22)
+    if host_pipeline:
+        a0 = a1 = None
+        n = x0.numel
+    else:
+        a0, a1 = _flat(x0.data), _flat(x1.data)
+        n = a0.numel()
     levels = prefix_levels(w)
     need = {(BOOL, w): n * (1 + 2 * levels), (ARITH, N): (1 if drelu_only else 2) * n}
     s0.triples.check(need)
     s1.triples.check(need)
     views = [(s.triples.draw(BOOL, w, need[(BOOL, w)]), s.triples.draw(ARITH, N, need[(ARITH, N)])) for s in (s0, s1)]
-    y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
-    y1 = torch.empty(n, dtype=torch.int64, device=a0.device)
-    _lib.call("hb_relu_pair", N, window.k, window.m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
-              views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(), int(drelu_only), _stream())
     for s in (s0, s1):
         for tag, nb in relu_trace(n, window, N, drelu_only):
             with s.endpoint.tag(tag):
                 s.endpoint.meter.record(nb)
+    if host_pipeline:
+        return _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only)
+    y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
+    y1 = torch.empty(n, dtype=torch.int64, device=a0.device)
+    _lib.call("hb_relu_pair", N, window.k, window.m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
+              views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(), int(drelu_only), _stream())
     return (_wrap(ArithShareTensor, 0, N, y0, x0.data, x0.shape), _wrap(ArithShareTensor, 1, N, y1, x1.data, x1.shape))
+
+
+_PIPE: dict = {}
+
+
+def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=1 << 21):
+    """Pinned host shares in/out: the layer goes through in chunks on three streams so the
+    H2D copy of chunk c+1, the fused kernel on chunk c and the D2H copy of chunk c-1 overlap
+    (PCIe is full duplex).  Same kernel, same triples, same shares as the one-shot path."""
+    dev = _dev.device()
+    if dev.index not in _PIPE:
+        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(3))
+    streams = _PIPE[dev.index]
+    h0, h1 = x0.data.reshape(-1), x1.data.reshape(-1)
+    d0, d1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
+    e0, e1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
+    o0, o1 = torch.empty(n, dtype=torch.int64, pin_memory=True), torch.empty(n, dtype=torch.int64, pin_memory=True)
+    cur = torch.cuda.current_stream()
+    lib = _lib.load()
+    for c, lo in enumerate(range(0, n, chunk)):
+        hi = min(n, lo + chunk)
+        st = streams[c % 3]
+        st.wait_stream(cur)
+        with torch.cuda.stream(st):
+            d0[lo:hi].copy_(h0[lo:hi], non_blocking=True)
+            d1[lo:hi].copy_(h1[lo:hi], non_blocking=True)
+            _lib.check(lib.hb_relu_pair_range(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(),
+                                              e0.data_ptr(), e1.data_ptr(), views[0][0].abi(), views[1][0].abi(),
+                                              views[0][1].abi(), views[1][1].abi(), int(drelu_only),
+                                              st.cuda_stream))
+            o0[lo:hi].copy_(e0[lo:hi], non_blocking=True)
+            o1[lo:hi].copy_(e1[lo:hi], non_blocking=True)
+    for st in streams:
+        st.synchronize()
+    return (ArithShareTensor(0, N, o0.reshape(x0.shape)), ArithShareTensor(1, N, o1.reshape(x1.shape)))

@@ -198,3 +198,55 @@ def test_dist_endpoint_gloo_world2():
     assert res[0][0] == [bytes([1]) * 8, bytes([1]) * 16, bytes([1]) * 24]
     assert res[1][0] == [bytes([0]) * 8, bytes([0]) * 16, bytes([0]) * 24]
     assert res[0][1]["tags"]["Circuit"] == {"bytes": 48, "rounds": 3}
+
+
+class _WireOverEndpoint:
+    """Oracle party logic (Wire.swap + tag) on top of one of this package's endpoints."""
+
+    def __init__(self, ep):
+        self.ep, self.tag, self.trace = ep, "Other", []
+
+    def swap(self, payload: bytes) -> bytes:
+        with self.ep.tag(self.tag):
+            got = self.ep.exchange(payload)
+        self.trace.append((self.tag, len(payload)))
+        return got
+
+
+def _dist_relu_worker(rank, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_cases as gc
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    case = next(c for c in gc.RELU_CASES if c["name"] == "base1001_22_16")
+    xs = gc.make_inputs(case)
+    w = case["k"] - case["m"]
+    curs = O.stocked_cursors(xs[0].size, w, 64, case["seed"])
+    ep = transport.DistEndpoint(rank, rank ^ 1)
+    y = O.p_relu(rank, _WireOverEndpoint(ep), curs[rank], xs[rank], 64, case["k"], case["m"])
+    q.put((rank, O.digest(y), [list(t) for t in ep.meter.trace]))
+    dist.destroy_process_group()
+
+
+def test_dist_relu_rounds_gloo_world2(golden):
+    """The N>1 transport path: two processes, one party each, every ReLU round a
+    torch.distributed send/recv (gloo here, NCCL on GPUs).  Shares and meter traces
+    equal the reference's."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_dist_relu_worker, args=(r, port, q)) for r in (0, 1)]
+    for p in ps:
+        p.start()
+    res = {r: (d, t) for r, d, t in (q.get(timeout=180) for _ in ps)}
+    for p in ps:
+        p.join(60)
+    g = golden[0]["base1001_22_16"]
+    assert res[0][0] == g["y0_sha"] and res[1][0] == g["y1_sha"]
+    assert res[0][1] == g["trace0"] and res[1][1] == g["trace1"]
