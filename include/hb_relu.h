@@ -126,6 +126,7 @@ int hb_beaver_close(int kind, int party, int w, int64_t count, const uint64_t* x
 #define HB_EW_OWNER 8     /* out = party == p ? a : 0                 protocol.py:153-156 */
 #define HB_EW_STACK2 9    /* out = [a ; a] */
 #define HB_EW_MASKW 10    /* out = a & mask(w) */
+#define HB_EW_DRELU_SHARES 11 /* out = 1 - msb(((a>>p)&m) + ((b>>p)&m)), w = k - m, p = m  simulator.py:33-44 */
 int hb_ewise(int op, int party, int w, int64_t count, int p, const uint64_t* a, const uint64_t* b, uint64_t* out,
              uint64_t* out2, void* stream);
 /* 1 if any word > 1 (b2a_bit precondition, protocol.py:166-167); synchronises `stream` */

@@ -25,7 +25,7 @@ HB_OK, HB_ERR_CUDA, HB_ERR_CONFIG, HB_ERR_TRANSPORT, HB_ERR_DATA, HB_ERR_TRIPLES
 TAG_BY_CODE = {0: "Circuit", 1: "Mult", 2: "B2A", 3: "Other"}
 
 EW = dict(SLICE=0, MSB=1, XOR=2, KS_RHS=3, KS_UPDATE=4, KS_FINISH=5, B2A_LIFT=6, DRELU_OUT=7, OWNER=8,
-          STACK2=9, MASKW=10)
+          STACK2=9, MASKW=10, DRELU_SHARES=11)
 
 u64p = ctypes.c_void_p
 i64 = ctypes.c_int64

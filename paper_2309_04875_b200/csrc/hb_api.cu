@@ -371,7 +371,7 @@ int hb_beaver_close(int kind, int party, int w, int64_t count, const uint64_t* x
 int hb_ewise(int op, int party, int w, int64_t count, int p, const uint64_t* a, const uint64_t* b, uint64_t* out,
              uint64_t* out2, void* stream) {
   if (w < 1 || w > 64) return fail(HB_ERR_CONFIG, "width must be in 1..64, got %d", w);
-  if (op < HB_EW_SLICE || op > HB_EW_MASKW) return fail(HB_ERR_CONFIG, "unknown elementwise op %d", op);
+  if (op < HB_EW_SLICE || op > HB_EW_DRELU_SHARES) return fail(HB_ERR_CONFIG, "unknown elementwise op %d", op);
   return cuda_status(hb_ops_ewise(op, party, w, (u64)count, p, a, b, out, out2, S(stream)), "hb_ewise");
 }
 

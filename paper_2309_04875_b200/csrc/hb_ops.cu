@@ -113,6 +113,7 @@ enum EwOp {
   EW_OWNER = 8,      // out = a if party == p else 0  (a2b / b2a operand split)  protocol.py:153-156
   EW_STACK2 = 9,     // out = [a ; a]
   EW_MASKW = 10,     // out = a & mask(w)
+  EW_DRELU_SHARES = 11,  // out = 1 - msb((a>>p & mk) + (b>>p & mk)), the plaintext sign oracle  simulator.py:33-44
 };
 
 __global__ void k_ewise(int op, int party, int w, u64 n, int p, const u64* __restrict__ a, const u64* __restrict__ b,
@@ -143,6 +144,7 @@ __global__ void k_ewise(int op, int party, int w, u64 n, int p, const u64* __res
     case EW_OWNER: out[i] = (party == p) ? (a[i] & mk) : 0ull; break;
     case EW_STACK2: out[i] = a[i]; out[n + i] = a[i]; break;
     case EW_MASKW: out[i] = a[i] & mk; break;
+    case EW_DRELU_SHARES: out[i] = 1ull - (((((a[i] >> p) & mk) + ((b[i] >> p) & mk)) & mk) >> (w - 1)); break;
   }
 }
 

@@ -187,6 +187,14 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
         }
       }
     }
+    // weight-limb tile loads go out together with the patch loads (<= 2 int4 per thread)
+    const int n16 = J * NT * KB / 16;
+    int4 wv[2];
+    {
+      const int4* src = reinterpret_cast<const int4*>(A.wl + ((long long)ntile * nkb + kb) * J * NT * KB);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) wv[u] = (tid + u * TPB < n16) ? __ldg(src + tid + u * TPB) : make_int4(0, 0, 0, 0);
+    }
     if (kb >= 2) {  // the MMAs that read this stage (block kb-2) must be done
       mbar_wait(&bar_empty[st], phase[st]);
       phase[st] ^= 1;
@@ -207,13 +215,10 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
         *reinterpret_cast<uint4*>(sA + (4 + i) * PLANE + off) = make_uint4(hi[0][i], hi[1][i], hi[2][i], hi[3][i]);
       }
     }
-    // ---- B: weight limb tiles are pre-laid out; plain 16-byte copies
-    {
-      const int4* src = reinterpret_cast<const int4*>(A.wl + ((long long)ntile * nkb + kb) * J * NT * KB);
-      int4* dst = reinterpret_cast<int4*>(sB);
-      const int n16 = J * NT * KB / 16;
-      for (int k = tid; k < n16; k += TPB) dst[k] = __ldg(src + k);
-    }
+    // ---- B: this thread's share of the pre-laid-out weight-limb tile (loaded above)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (tid + u * TPB < n16) reinterpret_cast<int4*>(sB)[tid + u * TPB] = wv[u];
     fence_async_smem();
     __syncthreads();
     // ---- MMA issue (one thread): 2 K-steps x all limb pairs with i + j <= 7

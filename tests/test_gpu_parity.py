@@ -300,3 +300,31 @@ def test_stock_on_device_matches_reference_stream():
     va, vb = a.draw("bool", 8, 10_000), b.draw("bool", 8, 10_000)
     for x, y in zip(va.unpacked(), vb.unpacked()):
         assert np.array_equal(x, y)
+
+
+def test_gpu_drelu_from_shares_and_sim_relu():
+    """simulator.drelu_from_shares on the GPU == the reference arithmetic (oracle), and the
+    protocol agrees with it element for element (test_simulator.py:70-88)."""
+    from paper_2309_04875_b200 import ring, simulator
+    from paper_2309_04875_b200.ring import FixedPointConfig
+
+    for (k, m) in ((21, 7), (64, 0), (22, 14), (10, 3)):
+        x0, x1 = gc.baseline_inputs(1 << 16, seed=k)
+        got = simulator.drelu_from_shares(x0, x1, 64, BitWindow(k, m))
+        assert np.array_equal(got, O.drelu_from_shares(x0, x1, 64, k, m))
+    case = next(c for c in gc.RELU_CASES if c["name"] == "sim10k_21_7")
+    x0, x1 = gc.make_inputs(case)
+    s0, s1, eps = stocked_sessions_for_relu(x0.size, 14, 64)
+    r0, r1 = transport.run_parties(lambda: protocol.relu(s0, ArithShareTensor(0, 64, x0), BitWindow(21, 7)),
+                                   lambda: protocol.relu(s1, ArithShareTensor(1, 64, x1), BitWindow(21, 7)),
+                                   endpoints=eps)
+    keep = simulator.drelu_from_shares(x0, x1, 64, BitWindow(21, 7))
+    e = (x0 + x1)
+    assert np.array_equal(sharing.reconstruct_arith(r0, r1), ring.mul_mod(e, keep, 64))
+    cfg = FixedPointConfig(64, 16)
+    xf = np.linspace(-5, 5, 101)
+    out = simulator.sim_relu(xf, BitWindow(20, 6), cfg, np.random.default_rng(6))
+    e2 = ring.encode_array(xf, cfg)
+    t0, t1 = sharing.share_arith(e2, 64, np.random.default_rng(6))
+    ref_keep = O.drelu_from_shares(t0.data, t1.data, 64, 20, 6)
+    assert np.array_equal(out != 0.0, (ref_keep == 1) & (xf != 0.0))
