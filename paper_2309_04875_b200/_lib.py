@@ -114,6 +114,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                 fn.restype = res
                 fn.argtypes = args
             _lib = lib
+            if hasattr(lib, "hb_debug_conv_stamps"):
+                lib.hb_debug_conv_stamps.restype = ctypes.c_int
     return _lib
 
 

@@ -18,6 +18,9 @@ struct ConvArgs {
   int party, frac;
   const u64* bias;     // [N] (party 0) or null
   u64* y;              // NCHW [B][N][OH*OW]
+  int nstage;          // smem pipeline depth (set by hb_tc_conv)
+  int dbg;             // profiling switches (HB_TC_DEBUG): 1 = no MMAs, 2 = no global gathers, 4 = timestamps
+  long long* stamps;   // dbg & 4: per-CTA clock64 phase stamps [grid][8]
 };
 
 }  // namespace tc
