@@ -14,7 +14,7 @@
 // CTA: 128 threads, output tile 128 rows (M = batch*OH*OW) x N_T columns.
 //   mainloop, per K block of 64:  all threads gather the im2col patch values of
 //   the tile (u64), split them into 8 limb planes and store them in shared memory
-//   in the UMMA canonical K-major no-swizzle layout (8x16B core matrices); the
+//   in the UMMA K-major SWIZZLE_64B layout (64-byte rows, 16-byte chunks XOR-swizzled); the
 //   weight-limb tile is copied as-is (host pre-lays it out).  One elected thread
 //   issues the MMAs and tcgen05.commit's a per-stage mbarrier; two stages, so the
 //   gather of block k+1 overlaps the tensor-core work of block k.
@@ -39,11 +39,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (canonical layout
-// ((8,m),(T,2)):((1T,SBO),(1,LBO)) in 16-byte units; cute mma_traits_sm100.hpp)
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1 (sm100)
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes, 8-row atoms of 512 B
+// (SBO), 16-byte chunk index XOR (row >> 1) & 3 (cute Swizzle<2,4,3>); LBO unused for swizzled
+// K-major; version 1 (sm100); layout type 4 = SWIZZLE_64B (cute mma_sm100_desc.hpp).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) |
+         (4ull << 61);
 }
 
 // instruction descriptor: D s32, A u8, B s8, both K-major, M = 128, N = n
@@ -100,8 +101,8 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
-// canonical K-major offset of (row r, K byte c) inside one [rows x 64 B] tile
-__device__ __forceinline__ int canon(int r, int c) { return (r >> 3) * 512 + (c >> 4) * 128 + (r & 7) * 16 + (c & 15); }
+// SWIZZLE_64B K-major offset of (row r, K byte c) inside one [rows x 64 B] tile
+__device__ __forceinline__ int canon(int r, int c) { return r * 64 + ((((c >> 4) ^ (r >> 1)) & 3) << 4) + (c & 15); }
 
 
 // 4x4 byte transpose: out[i] = byte i of (w0, w1, w2, w3), packed little-endian
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
   if (warp == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(&bar_full[i], NPROD);
+      mbar_init(&bar_full[i], NPROD / 32);  // one arrival per producer warp
       mbar_init(&bar_empty[i], 1);
     }
     mbar_init(&bar_done, 1);
@@ -179,8 +180,8 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
               if (sh > 7) continue;
               const int first_i = sh - (J - 1) > 0 ? sh - (J - 1) : 0;
               const uint32_t acc = (kb == 0 && ks == 0 && i == first_i) ? 0u : 1u;
-              const uint64_t da = sdesc(aBase + i * PLANE + ks * 256, 128, 512);
-              const uint64_t db = sdesc(bBase + j * NT * KB + ks * 256, 128, 512);
+              const uint64_t da = sdesc(aBase + i * PLANE + ks * 32);
+              const uint64_t db = sdesc(bBase + j * NT * KB + ks * 32);
               mma_i8(tmem + sh * NT, da, db, idesc_i8(NT), acc);
             }
           }
@@ -193,8 +194,10 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
       __syncwarp();
     }
   } else {
-    // ================= producers: row r = tid / 4, K bytes [16q, 16q + 16) of each block
-    const int r = tid >> 2, q = tid & 3;
+    // ================= producers: thread (r, q) owns row r, K bytes [16q, 16q + 16) of each block.
+    // r & 7 = tid & 7: each 8-thread phase of a 128-bit smem store covers 8 rows of one 512-byte
+    // swizzle atom, whose XOR spreads them over all 32 banks; consecutive threads = consecutive pixels.
+    const int r = ((tid >> 5) << 3) | (tid & 7), q = (tid >> 3) & 3;
     const long long m = m0 + r;
     const bool row_ok = m < A.M;
     const long long S = (long long)A.OH * A.OW;
@@ -212,33 +215,38 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
     const int4* wsrc = reinterpret_cast<const int4*>(A.wl) + (long long)ntile * nkb * n16;
     const int off = canon(r, q * 16);
 
+    // 16 patch values (k = c*khw + ki*kw + kj) of block kb for this thread
+    auto gather = [&](int kb, u64 (&v)[16]) {
+      const int k0 = kb * KB + q * 16;
+      int c = k0 / khw;
+      const int t0 = k0 - c * khw;
+      int ki = t0 / A.kw, kj = t0 - ki * A.kw;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int ih = ih0 + ki, iw = iw0 + kj;
+        const bool ok = !(A.dbg & 2) && row_ok && (k0 + e < A.K) && (unsigned)ih < (unsigned)A.H &&
+                        (unsigned)iw < (unsigned)A.W;
+        v[e] = ok ? (u64)__ldg(reinterpret_cast<const unsigned long long*>(xb + c * HW + (long long)ih * A.W + iw))
+                  : 0ull;
+        if (++kj == A.kw) {
+          kj = 0;
+          if (++ki == A.kh) {
+            ki = 0;
+            ++c;
+          }
+        }
+      }
+    };
+
+    u64 v[16];
+    gather(0, v);
     for (int kb = 0; kb < nkb; ++kb) {
       const int st = kb % NSTAGE;
       uint8_t* sA = smem + st * stage_bytes;
       uint8_t* sB = sA + 8 * PLANE;
-      // loads first: 16 patch values (k = c*khw + ki*kw + kj) and this thread's weight-tile share
-      u64 v[16];
-      {
-        const int k0 = kb * KB + q * 16;
-        int c = k0 / khw;
-        const int t0 = k0 - c * khw;
-        int ki = t0 / A.kw, kj = t0 - ki * A.kw;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int ih = ih0 + ki, iw = iw0 + kj;
-          const bool ok = !(A.dbg & 2) && row_ok && (k0 + e < A.K) && (unsigned)ih < (unsigned)A.H &&
-                          (unsigned)iw < (unsigned)A.W;
-          v[e] = ok ? (u64)__ldg(reinterpret_cast<const unsigned long long*>(xb + c * HW + (long long)ih * A.W + iw))
-                    : 0ull;
-          if (++kj == A.kw) {
-            kj = 0;
-            if (++ki == A.kh) {
-              ki = 0;
-              ++c;
-            }
-          }
-        }
-      }
+      // software pipeline: the next block's gathers are in flight while this block is split
+      u64 nv[16];
+      if (kb + 1 < nkb) gather(kb + 1, nv);
       int4 wv[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
@@ -261,7 +269,10 @@ __global__ void __launch_bounds__(TPB, 1) k_conv_tc(const ConvArgs A) {
       for (int u = 0; u < 2; ++u)
         if (tid + u * NPROD < n16) reinterpret_cast<int4*>(sB)[tid + u * NPROD] = wv[u];
       fence_async_smem();
-      mbar_arrive(&bar_full[st]);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bar_full[st]);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = nv[e];
     }
 
     if (stamp && tid == 0) my_st[2] = clock64();

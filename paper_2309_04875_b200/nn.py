@@ -269,15 +269,19 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
 
 
 def _tc_tiles(limbs, n, k, nt, kp):
-    """Weight limbs in the tensor-core kernel's order [n tile][k block of 64][limb][UMMA canonical
-    K-major tile: (row>>3, k>>4, row&7, k&15)] (hb_ring_tc.cu)."""
+    """Weight limbs in the tensor-core kernel's order [n tile][k block of 64][limb][row][64 B],
+    each [rows x 64 B] tile in the UMMA K-major SWIZZLE_64B layout: 16-byte chunk c of row r
+    stored at chunk c ^ ((r >> 1) & 3) (hb_ring_tc.cu canon())."""
     j = len(limbs)
     ntiles = -(-n // nt)
     full = np.zeros((j, ntiles * nt, kp), dtype=np.int8)
     for jj, l in enumerate(limbs):
         full[jj, :n, :k] = l
-    t = full.reshape(j, ntiles, nt // 8, 8, kp // 64, 4, 16)        # j, tile, g, rr, kb, cc, e
-    return np.ascontiguousarray(t.transpose(1, 4, 0, 2, 5, 3, 6)).reshape(-1)  # tile, kb, j, g, cc, rr, e
+    t = full.reshape(j, ntiles, nt, kp // 64, 4, 16)                  # j, tile, row, kb, chunk, e
+    rows = np.arange(nt)
+    src_chunk = np.arange(4)[None, :] ^ ((rows[:, None] >> 1) & 3)  # stored chunk s holds chunk s ^ sw(r)
+    t = t[:, :, rows[:, None], :, src_chunk, :]                       # -> (row, s, j, tile, kb, e)
+    return np.ascontiguousarray(t.transpose(3, 4, 2, 0, 1, 5)).reshape(-1)  # tile, kb, j, row, s, e
 
 
 _WCACHE: dict = {}
