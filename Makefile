@@ -10,7 +10,7 @@ LIBDIR  := paper_2309_04875_b200/lib
 LIB     := $(LIBDIR)/libhbrelu.so
 
 WIDTH_TUS := $(wildcard $(CSRC)/hb_relu_w*.cu)
-SRCS      := $(CSRC)/hb_api.cu $(CSRC)/hb_ops.cu $(CSRC)/hb_ring.cu $(CSRC)/hb_ring_tc.cu $(CSRC)/hb_dealer.cu $(WIDTH_TUS)
+SRCS      := $(CSRC)/hb_api.cu $(CSRC)/hb_ops.cu $(CSRC)/hb_ring.cu $(CSRC)/hb_ring_tc.cu $(CSRC)/hb_conv_tma.cu $(CSRC)/hb_dealer.cu $(WIDTH_TUS)
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(CSRC)/hb_widths.inc include/hb_relu.h
 

@@ -12,6 +12,7 @@
 #include "../../include/hb_relu.h"
 #include "hb_relu_impl.cuh"
 #include "hb_ring_tc.cuh"
+#include "hb_conv_tma.cuh"
 
 using hb::u64;
 
@@ -457,6 +458,34 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
   A.y = y;
   if (A.M == 0) return HB_OK;
   return cuda_status(hb_tc_conv(A, n_tile, S(stream)), "hb_conv_limbs_tc");
+}
+
+int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int width, uint8_t* planes, void* stream) {
+  if (batch < 0 || channels <= 0 || height <= 0 || width <= 0) return fail(HB_ERR_CONFIG, "bad tensor geometry");
+  return cuda_status(hb_limbs_nhwc_launch(x, batch, channels, (long long)height * width, planes, S(stream)),
+                     "hb_limbs_nhwc");
+}
+
+int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
+                      int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
+                      int frac_bits, const uint64_t* bias, uint64_t* y, void* stream) {
+  if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
+    return fail(HB_ERR_CONFIG, "bad conv geometry");
+  if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
+  if (channels % 64) return fail(HB_ERR_CONFIG, "TMA conv needs channels %% 64 == 0, got %d", channels);
+  if (stride > 8 || (width + 2 * pad - kw) / stride + 1 > 256) return fail(HB_ERR_CONFIG, "stride / width out of range");
+  const int64_t K = (int64_t)channels * kh * kw;
+  if (K > 21900) return fail(HB_ERR_CONFIG, "K = %lld too large for exact int32 shift accumulators", (long long)K);
+  if (j_limbs < 1 || j_limbs > 3) return fail(HB_ERR_CONFIG, "tensor-core path supports 1..3 weight limbs");
+  if (n_tile != 16 && n_tile != 32 && n_tile != 64) return fail(HB_ERR_CONFIG, "n_tile must be 16, 32 or 64");
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  int bb, bh, bw;
+  const int oh = (height + 2 * pad - kh) / stride + 1, ow = (width + 2 * pad - kw) / stride + 1;
+  if (hb_tma_conv_box(batch, oh, ow, &bb, &bh, &bw))
+    return fail(HB_ERR_CONFIG, "output %dx%d does not tile into 128-pixel boxes", oh, ow);
+  return cuda_status(hb_tma_conv(planes, batch, channels, height, width, kh, kw, stride, pad, wlimbs, n_out, j_limbs,
+                                 n_tile, party, frac_bits, bias, y, S(stream)),
+                     "hb_conv_limbs_tma");
 }
 
 int hb_deal_triples(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int kind, int width,

@@ -1,0 +1,382 @@
+// hb_conv_tma.cu -- ring-exact conv / linear as an implicit GEMM fed by TMA (sm_100a).
+//
+// y = trunc( (patches(x) W^T) mod 2^64 ) + [p0] b   for a uint64 share x (nn.py:198-243).
+//
+// Two kernels:
+//
+// k_limbs_nhwc   NCHW uint64 share -> 8 byte-limb planes [limb][B][H][W][C] (uint8, channels
+//                innermost).  HBM-bound: 8 B read + 8 B written per element.  Through a
+//                64-channel x 32-pixel shared-memory tile (XOR-swizzled, conflict-free), 8x8
+//                byte transposes, 64-byte coalesced channel runs on the store side.
+//
+// k_conv_tma<NT> persistent, warp-specialised tcgen05 implicit GEMM.  Output tile = 128
+//                output pixels (rows; a (batch, oh, ow) box) x NT output channels.  The K loop
+//                runs over (tap ki,kj) x (64-channel chunk): for each K block ONE 5-D TMA
+//                (channels, ow, oh, batch, limb) brings the 8 limb tiles of the shifted input
+//                window (zero-filled outside the image = the conv padding; traversal stride =
+//                the conv stride) into shared memory in the UMMA K-major SWIZZLE_64B layout,
+//                and one bulk copy brings the J weight-limb tiles (pre-laid out on the host).
+//                  warp 4  TMA producer (one elected lane), up to NSTAGE K blocks ahead
+//                  warp 5  MMA issuer: tcgen05.mma.kind::i8 u8 x s8 -> s32, M=128.  Products
+//                          x_i w_j with the same byte shift s = i + j accumulate in the SAME
+//                          TMEM columns [s*NT, s*NT + NT): with the J weight tiles stacked
+//                          along N, limb i is ONE MMA of N = min(J, 8 - i)*NT writing shifts
+//                          i .. i+J-1 at once (8 MMAs per K=32 step instead of up to 21).
+//                  warps 0-3 epilogue: tcgen05.ld the 8 shift accumulators of their TMEM lane
+//                          quarter, fold sum_s acc_s 2^(8s) mod 2^64, SecureML local truncation
+//                          (party-dependent), party-0 bias, NCHW store (lanes = consecutive pixels).
+//                TMEM holds 8*NT columns (512 at NT = 64): one tile per SM; the producer runs
+//                ahead into the next tile while the epilogue drains the accumulators.
+//
+// Exactness: |acc_s| <= 3 * K * 255 * 128 < 2^31 for K <= 21900 (ResNet max K = 4608); all
+// other arithmetic is mod 2^64.  The K order (ki, kj, c) differs from the reference's im2col
+// order (c, ki, kj) -- integer sums, so the result is identical.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "hb_common.cuh"
+#include "hb_conv_tma.cuh"
+#include "hb_tc_ptx.cuh"
+
+namespace hb {
+namespace tc {
+
+// ------------------------------------------------------------------ limb planes (NHWC)
+
+constexpr int LP_C = 64, LP_P = 32;  // channels x pixels per CTA tile
+
+__global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, long long B, int C, long long HW,
+                                                    uint8_t* __restrict__ planes) {
+  __shared__ u64 tile[LP_C * LP_P];
+  const long long P = B * HW;                  // (batch, pixel) rows
+  const long long q0 = (long long)blockIdx.x * LP_P;
+  const int c0 = blockIdx.y * LP_C;
+  const int tid = threadIdx.x;
+  // load: warp = 32 consecutive rows of one channel (coalesced along the pixels)
+#pragma unroll
+  for (int r = 0; r < LP_C * LP_P / 256; ++r) {
+    const int idx = tid + r * 256, c = idx >> 5, qq = idx & 31;
+    const long long q = q0 + qq;
+    u64 v = 0;
+    if (q < P && c0 + c < C) {
+      const long long b = q / HW, p = q - b * HW;
+      v = x[(b * C + c0 + c) * HW + p];
+    }
+    tile[c * LP_P + (qq ^ ((c >> 3) << 2))] = v;
+  }
+  __syncthreads();
+  // store: thread (g = 8 channels, row qq): 8x8 byte transpose, one 8-byte store per limb;
+  // a warp writes 4 rows x 64 contiguous channel bytes per limb
+  const int g = tid & 7, qq = tid >> 3;
+  const long long q = q0 + qq;
+  if (q >= P) return;
+  uint32_t lo03[4], lo47[4], hi03[4], hi47[4];
+  u64 v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = g * 8 + e;
+    v[e] = tile[c * LP_P + (qq ^ ((c >> 3) << 2))];
+  }
+  bytes_t4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3], lo03);
+  bytes_t4((uint32_t)v[4], (uint32_t)v[5], (uint32_t)v[6], (uint32_t)v[7], lo47);
+  bytes_t4((uint32_t)(v[0] >> 32), (uint32_t)(v[1] >> 32), (uint32_t)(v[2] >> 32), (uint32_t)(v[3] >> 32), hi03);
+  bytes_t4((uint32_t)(v[4] >> 32), (uint32_t)(v[5] >> 32), (uint32_t)(v[6] >> 32), (uint32_t)(v[7] >> 32), hi47);
+  const long long plane = P * C;
+  const int c = c0 + g * 8;
+  if (c + 8 <= C) {
+    uint8_t* dst = planes + q * C + c;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      *reinterpret_cast<uint2*>(dst + i * plane) = make_uint2(lo03[i], lo47[i]);
+      *reinterpret_cast<uint2*>(dst + (4 + i) * plane) = make_uint2(hi03[i], hi47[i]);
+    }
+  } else {
+    for (int e = 0; e < 8 && c + e < C; ++e)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) planes[i * plane + q * C + c + e] = (uint8_t)(v[e] >> (8 * i));
+  }
+}
+
+// ------------------------------------------------------------------ implicit-GEMM conv
+
+constexpr int TMA_THREADS = 192;  // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int TMA_MAX_STAGE = 4;
+
+template <int NT>
+__global__ void __launch_bounds__(TMA_THREADS, 1)
+    k_conv_tma(const __grid_constant__ CUtensorMap tmap, const TmaConvArgs A) {
+  constexpr int TMEM_COLS = 8 * NT < 32 ? 32 : 8 * NT;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // stage buffers 1024-aligned (SWIZZLE_64B atoms and TMA destinations)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_full[TMA_MAX_STAGE], bar_empty[TMA_MAX_STAGE], bar_tfull, bar_tempty;
+  __shared__ uint32_t tmem_base_s;
+
+  const int J = A.J, NS = A.nstage, nkb = A.nkb;
+  const int bbytes = J * NT * KB;                 // weight tiles per stage
+  const int stage_bytes = 8 * PLANE + bbytes;     // multiple of 1024
+  const uint32_t tx_bytes = (uint32_t)stage_bytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 5) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_empty[i], 1);
+    }
+    mbar_init(&bar_tfull, 1);
+    mbar_init(&bar_tempty, 4);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 4 && lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int S = A.OH * A.OW;
+
+  if (warp == 4) {
+    // ================= TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
+        const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+        const long long m0 = (long long)mt * BM;
+        const int b0 = (int)(m0 / S), rem = (int)(m0 - (long long)b0 * S);
+        const int oh0 = rem / A.OW, ow0 = rem - (rem / A.OW) * A.OW;
+        const int8_t* wsrc = A.wl + (long long)ntile * nkb * bbytes;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % NS;
+          if (it >= NS) mbar_wait(&bar_empty[st], ((it / NS) - 1) & 1);
+          const int tap = kb / A.ncc, cc = kb - tap * A.ncc;
+          const int ki = tap / A.kw, kj = tap - ki * A.kw;
+          uint8_t* sA = smem + st * stage_bytes;
+          mbar_expect_tx(&bar_full[st], tx_bytes);
+          tma_load_5d(sA, &tmap, cc * KB, ow0 * A.stride - A.pad + kj, oh0 * A.stride - A.pad + ki, b0, 0,
+                      &bar_full[st]);
+          bulk_load(sA + 8 * PLANE, wsrc + (long long)kb * bbytes, (uint32_t)bbytes, &bar_full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ================= MMA issuer
+    int it = 0, lt = 0;
+    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
+      if (lt > 0) mbar_wait(&bar_tempty, (lt - 1) & 1);  // epilogue drained the accumulators
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int st = it % NS;
+        mbar_wait(&bar_full[st], (it / NS) & 1);
+        tc_fence_after();
+        if (lane == 0 && !(A.dbg & 1)) {
+          const uint32_t aBase = smem_u32(smem + st * stage_bytes), bBase = aBase + 8 * PLANE;
+#pragma unroll
+          for (int ks = 0; ks < KB / 32; ++ks) {
+            if (kb == 0 && ks == 0) {
+              // first K step: one MMA per (i, j) so every shift accumulator starts with acc = 0
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                for (int j = 0; j < J && i + j < 8; ++j) {
+                  const int sh = i + j, first_i = sh - (J - 1) > 0 ? sh - (J - 1) : 0;
+                  mma_i8(tmem + sh * NT, sdesc(aBase + i * PLANE), sdesc(bBase + j * NT * KB), idesc_i8(NT),
+                         i == first_i ? 0u : 1u);
+                }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int nj = J < 8 - i ? J : 8 - i;
+                mma_i8(tmem + i * NT, sdesc(aBase + i * PLANE + ks * 32), sdesc(bBase + ks * 32), idesc_i8(nj * NT),
+                       1u);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mma_commit(&bar_empty[st]);  // stage free once these MMAs complete
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&bar_tfull);
+      __syncwarp();
+    }
+  } else {
+    // ================= epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
+    int lt = 0;
+    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
+      const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+      const long long em = (long long)mt * BM + warp * 32 + lane;
+      const bool eok = em < A.M;
+      const int eb = eok ? (int)(em / S) : 0;
+      const long long esp = eok ? em - (long long)eb * S : 0;
+      const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+      mbar_wait(&bar_tfull, lt & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += 8) {
+        uint32_t vv[8][8];
+#pragma unroll
+        for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
+        tmem_wait_ld();
+        if (c0 + 8 >= NT) {  // accumulators drained: let the next tile's MMAs start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_tempty);
+        }
+        u64 acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = 0;
+#pragma unroll
+        for (int sh = 0; sh < 8; ++sh)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
+        if (eok) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int n = ntile * NT + c0 + k;
+            if (n < A.N) {
+              u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+              if (A.party == 0 && A.bias) yv += A.bias[n];
+              A.y[((long long)eb * A.N + n) * S + esp] = yv;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+}  // namespace tc
+}  // namespace hb
+
+// ------------------------------------------------------------------ host side
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+}  // namespace
+
+cudaError_t hb_limbs_nhwc_launch(const uint64_t* x, long long B, int C, long long HW, uint8_t* planes,
+                                 cudaStream_t s) {
+  const long long P = B * HW;
+  if (P == 0) return cudaSuccess;
+  dim3 grid((unsigned)((P + hb::tc::LP_P - 1) / hb::tc::LP_P), (unsigned)((C + hb::tc::LP_C - 1) / hb::tc::LP_C));
+  hb::tc::k_limbs_nhwc<<<grid, 256, 0, s>>>(x, B, C, HW, planes);
+  return cudaGetLastError();
+}
+
+// returns 0 and fills the tile box when the output geometry tiles into 128-row (batch, oh, ow) boxes
+int hb_tma_conv_box(int B, int OH, int OW, int* bb, int* bh, int* bw) {
+  (void)B;
+  if (OW >= 128) {
+    if (OW % 128) return -1;
+    *bw = 128, *bh = 1, *bb = 1;
+    return 0;
+  }
+  if (128 % OW) return -1;
+  *bw = OW;
+  const int rows = 128 / OW;
+  if (OH >= rows) {
+    if (OH % rows) return -1;
+    *bh = rows, *bb = 1;
+    return 0;
+  }
+  if (rows % OH) return -1;
+  *bh = OH, *bb = rows / OH;
+  return 0;
+}
+
+cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
+                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias, uint64_t* y,
+                        cudaStream_t s) {
+  using namespace hb::tc;
+  auto encode = encode_fn();
+  if (!encode) return cudaErrorNotSupported;
+  TmaConvArgs A;
+  A.OH = (H + 2 * pad - kh) / stride + 1;
+  A.OW = (W + 2 * pad - kw) / stride + 1;
+  A.M = (long long)B * A.OH * A.OW;
+  if (A.M == 0) return cudaSuccess;
+  int bb, bh, bw;
+  if (hb_tma_conv_box(B, A.OH, A.OW, &bb, &bh, &bw)) return cudaErrorInvalidValue;
+  A.N = N;
+  A.J = J;
+  A.stride = stride;
+  A.pad = pad;
+  A.kw = kw;
+  A.ncc = C / KB;
+  A.nkb = kh * kw * A.ncc;
+  A.tiles_n = (N + nt - 1) / nt;
+  A.tiles = (int)((A.M + BM - 1) / BM) * A.tiles_n;
+  A.wl = wl;
+  A.party = party;
+  A.frac = frac;
+  A.bias = bias;
+  A.y = y;
+  static const int dbg = [] {
+    const char* e = getenv("HB_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  A.dbg = dbg;
+  const int stage_bytes = 8 * PLANE + J * nt * KB;
+  int ns = (227 * 1024 - 1024) / stage_bytes;
+  A.nstage = ns > TMA_MAX_STAGE ? TMA_MAX_STAGE : ns;
+  if (A.nstage < 2) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)A.nstage * stage_bytes + 1024;
+
+  // [limb][B][H][W][C] uint8, box (64 channels, bw*stride, bh*stride, bb, 8 limbs), traversal stride = conv stride
+  CUtensorMap tmap;
+  const cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, 8};
+  const cuuint64_t strides[4] = {(cuuint64_t)C, (cuuint64_t)W * C, (cuuint64_t)H * W * C,
+                                 (cuuint64_t)B * H * W * C};
+  const cuuint32_t box[5] = {(cuuint32_t)KB, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bb, 8};
+  const cuuint32_t estr[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
+  if (box[1] > 256 || box[2] > 256) return cudaErrorInvalidValue;
+  CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const int grid = A.tiles < sm_count() ? A.tiles : sm_count();
+  cudaError_t e;
+  switch (nt) {
+#define HB_NT(NT_)                                                                                      \
+  case NT_:                                                                                             \
+    e = cudaFuncSetAttribute(k_conv_tma<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                     \
+    k_conv_tma<NT_><<<grid, TMA_THREADS, smem, s>>>(tmap, A);                                           \
+    break;
+    HB_NT(16)
+    HB_NT(32)
+    HB_NT(64)
+#undef HB_NT
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}

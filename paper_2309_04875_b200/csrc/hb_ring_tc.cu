@@ -27,101 +27,17 @@
 
 #include "hb_common.cuh"
 #include "hb_ring_tc.cuh"
+#include "hb_tc_ptx.cuh"
 
 namespace hb {
 namespace tc {
 
-constexpr int BM = 128;   // rows per CTA = TMEM lanes
-constexpr int KB = 64;    // K bytes per stage (2 MMAs of K = 32)
-constexpr int PLANE = BM * KB;  // bytes per limb plane per stage (8 KB)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes, 8-row atoms of 512 B
-// (SBO), 16-byte chunk index XOR (row >> 1) & 3 (cute Swizzle<2,4,3>); LBO unused for swizzled
-// K-major; version 1 (sm100); layout type 4 = SWIZZLE_64B (cute mma_sm100_desc.hpp).
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) |
-         (4ull << 61);
-}
-
-// instruction descriptor: D s32, A u8, B s8, both K-major, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_i8(int n) {
-  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar)));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
-}
-
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-
-template <int NCOL>
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)), "n"(NCOL));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-}
-
-template <int NCOL>
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOL));
-}
-
-// 8 consecutive 32-bit TMEM columns of this thread's lane
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-
 // SWIZZLE_64B K-major offset of (row r, K byte c) inside one [rows x 64 B] tile
 __device__ __forceinline__ int canon(int r, int c) { return r * 64 + ((((c >> 4) ^ (r >> 1)) & 3) << 4) + (c & 15); }
-
-
-// 4x4 byte transpose: out[i] = byte i of (w0, w1, w2, w3), packed little-endian
-__device__ __forceinline__ void bytes_t4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
-  const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
-  const uint32_t t2 = __byte_perm(w0, w1, 0x7362), t3 = __byte_perm(w2, w3, 0x7362);
-  o[0] = __byte_perm(t0, t1, 0x5410);
-  o[1] = __byte_perm(t0, t1, 0x7632);
-  o[2] = __byte_perm(t2, t3, 0x5410);
-  o[3] = __byte_perm(t2, t3, 0x7632);
-}
 
 constexpr int NPROD = 512;        // producer threads: 4 per accumulator row
 constexpr int TPB = NPROD + 32;   // + one MMA-issuer warp
 constexpr int MAX_STAGE = 3;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // Warp-specialised: warps 0..15 gather/split/store (and run the epilogue), warp 16
 // issues the MMAs.  Stages are handed over with full/empty mbarriers, so producer

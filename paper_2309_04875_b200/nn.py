@@ -19,6 +19,7 @@ reference lacks.  Every layer runs on the GPU:
 
 from __future__ import annotations
 
+import collections
 import json
 import os
 import time
@@ -226,6 +227,7 @@ class _LimbWeight:
     wl_tc: torch.Tensor | None = None  # int8 tiles for hb_conv_limbs_tc (None: not eligible)
     kp_tc: int = 0
     nt: int = 0
+    wl_tma: torch.Tensor | None = None  # int8 tiles for hb_conv_limbs_tma, K order (ki, kj, c)
 
 
 def _balanced_limbs(w: np.ndarray):
@@ -265,6 +267,14 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
         lw.nt = 64 if n >= 64 else (32 if n > 16 else 16)
         lw.kp_tc = -(-k // 64) * 64
         lw.wl_tc = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt, lw.kp_tc)).to(dev)
+        c = w.shape[1]
+        if c % 64 == 0:  # TMA path: 64-channel K blocks, tap-major K order
+            if w.ndim == 4:
+                kh, kw = w.shape[2], w.shape[3]
+                limbs_t = [l.reshape(n, c, kh, kw).transpose(0, 2, 3, 1).reshape(n, k) for l in limbs]
+            else:
+                limbs_t = limbs
+            lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt, k)).to(dev)
     return lw
 
 
@@ -297,19 +307,60 @@ def _weight(weight, bias, cfg) -> _LimbWeight:
     return hit[2]
 
 
-RING_GEMM = os.environ.get("HB_RING_GEMM", "tc")  # "tc" (hand-written tcgen05) or "cublaslt"
+# "tc": hand-written tcgen05 (TMA implicit GEMM where eligible, else the fused gather kernel);
+# "tcgather": always the gather kernel; "cublaslt": im2col + torch._int_mm + combine
+RING_GEMM = os.environ.get("HB_RING_GEMM", "tc")
 
 
 def _use_tc(lw: _LimbWeight) -> bool:
-    return RING_GEMM == "tc" and lw.wl_tc is not None
+    return RING_GEMM in ("tc", "tcgather") and lw.wl_tc is not None
+
+
+_PLANES: "collections.OrderedDict" = collections.OrderedDict()
+
+
+def _limb_planes(x_nchw: torch.Tensor, stream) -> torch.Tensor:
+    """NHWC byte-limb planes of a share (hb_limbs_nhwc), cached for the few most recent inputs so a
+    residual block's body conv and shortcut conv (same input) split it once.  The cache holds the
+    input tensor itself (its memory cannot be recycled while cached) and its version counter."""
+    key = id(x_nchw)
+    hit = _PLANES.get(key)
+    if hit is not None and hit[0] is x_nchw and hit[1] == x_nchw._version:
+        _PLANES.move_to_end(key)
+        return hit[2]
+    b, c, h, w = x_nchw.shape
+    planes = torch.empty(8 * b * h * w * c, dtype=torch.uint8, device=x_nchw.device)
+    _lib.call("hb_limbs_nhwc", x_nchw.data_ptr(), b, c, h, w, planes.data_ptr(), stream)
+    _PLANES[key] = (x_nchw, x_nchw._version, planes)
+    while len(_PLANES) > 4:
+        _PLANES.popitem(last=False)
+    return planes
+
+
+def _tma_box_ok(oh: int, ow: int) -> bool:
+    """Output geometry tiles into 128-pixel (batch, oh, ow) boxes (hb_tma_conv_box)."""
+    if ow >= 128:
+        return ow % 128 == 0
+    if 128 % ow:
+        return False
+    rows = 128 // ow
+    return oh % rows == 0 if oh >= rows else rows % oh == 0
 
 
 def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int) -> torch.Tensor:
-    """Fused tcgen05 kernel (hb_conv_limbs_tc): NCHW share in, NCHW [b, n, oh, ow] share out."""
+    """tcgen05 ring conv: NCHW share in, NCHW [b, n, oh, ow] share out.  TMA-fed implicit GEMM over
+    NHWC limb planes (hb_limbs_nhwc + hb_conv_limbs_tma) when the layer qualifies, else the fused
+    gather kernel (hb_conv_limbs_tc)."""
     b, c, h, w = x_nchw.shape
     kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
     out = torch.empty((b, lw.n, oh, ow), dtype=torch.int64, device=x_nchw.device)
+    if RING_GEMM == "tc" and lw.wl_tma is not None and stride <= 8 and _tma_box_ok(oh, ow) and b > 0:
+        s = _dev.stream_handle()
+        planes = _limb_planes(x_nchw, s)
+        _lib.call("hb_conv_limbs_tma", planes.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tma.data_ptr(),
+                  lw.n, lw.j, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
+        return out
     _lib.call("hb_conv_limbs_tc", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
               lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(),
               _dev.stream_handle())
