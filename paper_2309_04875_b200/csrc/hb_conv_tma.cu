@@ -16,15 +16,16 @@
 //                window (zero-filled outside the image = the conv padding; traversal stride =
 //                the conv stride) into shared memory in the UMMA K-major SWIZZLE_64B layout,
 //                and one bulk copy brings the J weight-limb tiles (pre-laid out on the host).
-//                  warp 4  TMA producer (one elected lane), up to NSTAGE K blocks ahead
-//                  warp 5  MMA issuer: tcgen05.mma.kind::i8 u8 x s8 -> s32, M=128.  Products
+//                  warp P  TMA producer (one elected lane), up to NSTAGE K blocks ahead
+//                  warp M  MMA issuer: tcgen05.mma.kind::i8 u8 x s8 -> s32, M=128.  Products
 //                          x_i w_j with the same byte shift s = i + j accumulate in the SAME
 //                          TMEM columns [s*NT, s*NT + NT): with the J weight tiles stacked
 //                          along N, limb i is ONE MMA of N = min(J, 8 - i)*NT writing shifts
 //                          i .. i+J-1 at once (8 MMAs per K=32 step instead of up to 21).
-//                  warps 0-3 epilogue: tcgen05.ld the 8 shift accumulators of their TMEM lane
-//                          quarter, fold sum_s acc_s 2^(8s) mod 2^64, SecureML local truncation
-//                          (party-dependent), party-0 bias, NCHW store (lanes = consecutive pixels).
+//                  warps 0-15 epilogue (4 per TMEM lane quarter, one column group each):
+//                          tcgen05.ld the 8 shift accumulators, fold sum_s acc_s 2^(8s) mod 2^64,
+//                          SecureML local truncation (party-dependent), party-0 bias, NCHW store
+//                          (lanes = consecutive pixels).
 //                TMEM holds 8*NT columns (512 at NT = 64): one tile per SM; the producer runs
 //                ahead into the next tile while the epilogue drains the accumulators.
 //
@@ -49,31 +50,30 @@ namespace tc {
 
 constexpr int LP_C = 64, LP_P = 32;  // channels x pixels per CTA tile
 
-__global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, long long B, int C, long long HW,
+__global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, long long B, int C, int HW,
                                                     uint8_t* __restrict__ planes) {
   __shared__ u64 tile[LP_C * LP_P];
-  const long long P = B * HW;                  // (batch, pixel) rows
-  const long long q0 = (long long)blockIdx.x * LP_P;
+  // CTA = (image b, 32 pixels of it) x 64 channels: no per-element divisions
+  const int tiles_img = (HW + LP_P - 1) / LP_P;
+  const long long b = blockIdx.x / tiles_img;
+  const int p0 = (int)(blockIdx.x - b * tiles_img) * LP_P;
   const int c0 = blockIdx.y * LP_C;
   const int tid = threadIdx.x;
-  // load: warp = 32 consecutive rows of one channel (coalesced along the pixels)
+  const long long P = B * HW;
+  const u64* xb = x + (b * C + c0) * (long long)HW + p0;
+  // load: warp = 32 consecutive pixels of one channel (coalesced)
 #pragma unroll
   for (int r = 0; r < LP_C * LP_P / 256; ++r) {
     const int idx = tid + r * 256, c = idx >> 5, qq = idx & 31;
-    const long long q = q0 + qq;
-    u64 v = 0;
-    if (q < P && c0 + c < C) {
-      const long long b = q / HW, p = q - b * HW;
-      v = x[(b * C + c0 + c) * HW + p];
-    }
+    const u64 v = (p0 + qq < HW && c0 + c < C) ? __ldg(reinterpret_cast<const unsigned long long*>(xb + (long long)c * HW + qq)) : 0ull;
     tile[c * LP_P + (qq ^ ((c >> 3) << 2))] = v;
   }
   __syncthreads();
   // store: thread (g = 8 channels, row qq): 8x8 byte transpose, one 8-byte store per limb;
   // a warp writes 4 rows x 64 contiguous channel bytes per limb
   const int g = tid & 7, qq = tid >> 3;
-  const long long q = q0 + qq;
-  if (q >= P) return;
+  if (p0 + qq >= HW) return;
+  const long long q = b * HW + p0 + qq;
   uint32_t lo03[4], lo47[4], hi03[4], hi47[4];
   u64 v[8];
 #pragma unroll
@@ -103,7 +103,9 @@ __global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, l
 
 // ------------------------------------------------------------------ implicit-GEMM conv
 
-constexpr int TMA_THREADS = 192;  // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int EPI_WARPS = 16;                       // 4 per TMEM lane quarter, each a column group
+constexpr int PROD_WARP = EPI_WARPS, MMA_WARP = EPI_WARPS + 1;
+constexpr int TMA_THREADS = (EPI_WARPS + 2) * 32;  // + TMA producer warp + MMA issuer warp
 constexpr int TMA_MAX_STAGE = 4;
 
 template <int NT>
@@ -122,24 +124,24 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
   const uint32_t tx_bytes = (uint32_t)stage_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  if (warp == 5) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+  if (warp == MMA_WARP) tmem_alloc<TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&bar_full[i], 1);
       mbar_init(&bar_empty[i], 1);
     }
     mbar_init(&bar_tfull, 1);
-    mbar_init(&bar_tempty, 4);  // one arrival per epilogue warp
+    mbar_init(&bar_tempty, EPI_WARPS);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 4 && lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+  if (warp == PROD_WARP && lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   const int S = A.OH * A.OW;
 
-  if (warp == 4) {
+  if (warp == PROD_WARP) {
     // ================= TMA producer
     if (lane == 0) {
       int it = 0;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_WARP) {
     // ================= MMA issuer
     int it = 0, lt = 0;
     for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
@@ -203,52 +205,62 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ================= epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
+    // ================= epilogue: warp w reads TMEM lane quarter w & 3 (tile rows [32q, 32q + 32)),
+    // column group w >> 2 (CPG of the NT columns, all 8 shift accumulators)
+    constexpr int CPG = NT / 4 < 8 ? 8 : NT / 4;
+    constexpr int NGRP = NT / CPG;
+    const int quarter = warp & 3, cgrp = warp >> 2;
     int lt = 0;
     for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
       const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
-      const long long em = (long long)mt * BM + warp * 32 + lane;
+      const long long em = (long long)mt * BM + quarter * 32 + lane;
       const bool eok = em < A.M;
       const int eb = eok ? (int)(em / S) : 0;
       const long long esp = eok ? em - (long long)eb * S : 0;
-      const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
       mbar_wait(&bar_tfull, lt & 1);
       tc_fence_after();
+      if (cgrp < NGRP) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < NT; c0 += 8) {
-        uint32_t vv[8][8];
+        for (int c0 = cgrp * CPG; c0 < (cgrp + 1) * CPG; c0 += 8) {
+          uint32_t vv[8][8];
 #pragma unroll
-        for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
-        tmem_wait_ld();
-        if (c0 + 8 >= NT) {  // accumulators drained: let the next tile's MMAs start
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_tempty);
-        }
-        u64 acc[8];
+          for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
+          tmem_wait_ld();
+          u64 acc[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = 0;
+          for (int k = 0; k < 8; ++k) acc[k] = 0;
 #pragma unroll
-        for (int sh = 0; sh < 8; ++sh)
+          for (int sh = 0; sh < 8; ++sh)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
-        if (eok) {
+            for (int k = 0; k < 8; ++k) acc[k] += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
+          if (c0 + 8 >= (cgrp + 1) * CPG) {  // this warp's accumulators drained
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_tempty);
+          }
+          if (eok) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int n = ntile * NT + c0 + k;
-            if (n < A.N) {
-              u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
-              if (A.party == 0 && A.bias) yv += A.bias[n];
-              A.y[((long long)eb * A.N + n) * S + esp] = yv;
+            for (int k = 0; k < 8; ++k) {
+              const int n = ntile * NT + c0 + k;
+              if (n < A.N) {
+                u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                if (A.party == 0 && A.bias) yv += A.bias[n];
+                A.y[((long long)eb * A.N + n) * S + esp] = yv;
+              }
             }
           }
         }
+      } else {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_tempty);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<TMEM_COLS>(tmem);
+  if (warp == MMA_WARP) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 }  // namespace tc
@@ -284,10 +296,10 @@ int sm_count() {
 
 cudaError_t hb_limbs_nhwc_launch(const uint64_t* x, long long B, int C, long long HW, uint8_t* planes,
                                  cudaStream_t s) {
-  const long long P = B * HW;
-  if (P == 0) return cudaSuccess;
-  dim3 grid((unsigned)((P + hb::tc::LP_P - 1) / hb::tc::LP_P), (unsigned)((C + hb::tc::LP_C - 1) / hb::tc::LP_C));
-  hb::tc::k_limbs_nhwc<<<grid, 256, 0, s>>>(x, B, C, HW, planes);
+  if (B * HW == 0) return cudaSuccess;
+  const long long tiles = B * ((HW + hb::tc::LP_P - 1) / hb::tc::LP_P);
+  dim3 grid((unsigned)tiles, (unsigned)((C + hb::tc::LP_C - 1) / hb::tc::LP_C));
+  hb::tc::k_limbs_nhwc<<<grid, 256, 0, s>>>(x, B, C, (int)HW, planes);
   return cudaGetLastError();
 }
 
