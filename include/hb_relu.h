@@ -178,15 +178,17 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
                      int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,
                      int frac_bits, const uint64_t* bias, uint64_t* y, void* stream);
 
-/* Byte-limb planes of an NCHW share for the TMA conv: planes[i][b][h][w][c] = byte i of
- * x[b][c][h][w] (uint8, channels innermost; 8 planes of batch*height*width*channels bytes).
+/* Byte-limb planes of an NCHW share for the TMA conv, channel-blocked NHWC:
+ * planes[i][c/64][b][h][w][c%64] = byte i of x[b][c][h][w] (uint8; channels % 64 == 0;
+ * 8 planes of batch*height*width*channels bytes).
  * Replaces the limb split inside the reference's uint64 matmul (nn.py:222). */
 int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int width, uint8_t* planes, void* stream);
 
 /* Ring conv/linear (nn.py:214-243 conv2d_forward / linear_forward + truncate_local nn.py:198-211) as a
  * TMA-fed tcgen05 implicit GEMM over the limb planes of hb_limbs_nhwc: same result as
  * hb_conv_limbs_tc.  wlimbs: int8 [ceil(n_out/n_tile)][kh*kw*channels/64][j_limbs][n_tile x 64
- * SWIZZLE_64B K-major tile], K order (ki, kj, c).  channels % 64 == 0; the output (OH, OW) must tile
+ * SWIZZLE_64B K-major tile], K order (ki, kj, c), n_tile in {16, 32, 64, 128} (128: two shift
+ * passes).  channels % 64 == 0; the output (OH, OW) must tile
  * into 128-pixel (batch, oh, ow) boxes (OW a divisor or multiple of 128, ...). */
 int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
                       int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,

@@ -462,6 +462,7 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
 
 int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int width, uint8_t* planes, void* stream) {
   if (batch < 0 || channels <= 0 || height <= 0 || width <= 0) return fail(HB_ERR_CONFIG, "bad tensor geometry");
+  if (channels % 64) return fail(HB_ERR_CONFIG, "limb planes need channels %% 64 == 0, got %d", channels);
   return cuda_status(hb_limbs_nhwc_launch(x, batch, channels, (long long)height * width, planes, S(stream)),
                      "hb_limbs_nhwc");
 }
@@ -477,7 +478,8 @@ int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height
   const int64_t K = (int64_t)channels * kh * kw;
   if (K > 21900) return fail(HB_ERR_CONFIG, "K = %lld too large for exact int32 shift accumulators", (long long)K);
   if (j_limbs < 1 || j_limbs > 3) return fail(HB_ERR_CONFIG, "tensor-core path supports 1..3 weight limbs");
-  if (n_tile != 16 && n_tile != 32 && n_tile != 64) return fail(HB_ERR_CONFIG, "n_tile must be 16, 32 or 64");
+  if (n_tile != 16 && n_tile != 32 && n_tile != 64 && n_tile != 128)
+    return fail(HB_ERR_CONFIG, "n_tile must be 16, 32, 64 or 128");
   if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
   int bb, bh, bw;
   const int oh = (height + 2 * pad - kh) / stride + 1, ow = (width + 2 * pad - kw) / stride + 1;

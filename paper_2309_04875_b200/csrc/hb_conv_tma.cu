@@ -4,15 +4,15 @@
 //
 // Two kernels:
 //
-// k_limbs_nhwc   NCHW uint64 share -> 8 byte-limb planes [limb][B][H][W][C] (uint8, channels
-//                innermost).  HBM-bound: 8 B read + 8 B written per element.  Through a
+// k_limbs_nhwc   NCHW uint64 share -> 8 byte-limb planes, channel-blocked NHWC:
+//                [limb][C/64][B][H][W][64] (uint8; C % 64 == 0).  HBM-bound: 8 B read + 8 B written per element.  Through a
 //                64-channel x 32-pixel shared-memory tile (XOR-swizzled, conflict-free), 8x8
 //                byte transposes, 64-byte coalesced channel runs on the store side.
 //
 // k_conv_tma<NT> persistent, warp-specialised tcgen05 implicit GEMM.  Output tile = 128
 //                output pixels (rows; a (batch, oh, ow) box) x NT output channels.  The K loop
 //                runs over (tap ki,kj) x (64-channel chunk): for each K block ONE 5-D TMA
-//                (channels, ow, oh, batch, limb) brings the 8 limb tiles of the shifted input
+//                (64 channels, ow, oh, chunk*B + batch, limb) brings the 8 limb tiles of the shifted input
 //                window (zero-filled outside the image = the conv padding; traversal stride =
 //                the conv stride) into shared memory in the UMMA K-major SWIZZLE_64B layout,
 //                and one bulk copy brings the J weight-limb tiles (pre-laid out on the host).
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, l
 #pragma unroll
   for (int r = 0; r < LP_C * LP_P / 256; ++r) {
     const int idx = tid + r * 256, c = idx >> 5, qq = idx & 31;
-    const u64 v = (p0 + qq < HW && c0 + c < C) ? __ldg(reinterpret_cast<const unsigned long long*>(xb + (long long)c * HW + qq)) : 0ull;
+    const u64 v = (p0 + qq < HW) ? __ldg(reinterpret_cast<const unsigned long long*>(xb + (long long)c * HW + qq)) : 0ull;
     tile[c * LP_P + (qq ^ ((c >> 3) << 2))] = v;
   }
   __syncthreads();
@@ -85,32 +85,322 @@ __global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, l
   bytes_t4((uint32_t)v[4], (uint32_t)v[5], (uint32_t)v[6], (uint32_t)v[7], lo47);
   bytes_t4((uint32_t)(v[0] >> 32), (uint32_t)(v[1] >> 32), (uint32_t)(v[2] >> 32), (uint32_t)(v[3] >> 32), hi03);
   bytes_t4((uint32_t)(v[4] >> 32), (uint32_t)(v[5] >> 32), (uint32_t)(v[6] >> 32), (uint32_t)(v[7] >> 32), hi47);
+  // blocked layout [limb][C/64][B*H*W][64]: a limb's 32 x 64-byte rows of this tile are contiguous
+  uint8_t* dst = planes + (long long)(c0 / LP_C) * P * LP_C + q * LP_C + g * 8;
   const long long plane = P * C;
-  const int c = c0 + g * 8;
-  if (c + 8 <= C) {
-    uint8_t* dst = planes + q * C + c;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      *reinterpret_cast<uint2*>(dst + i * plane) = make_uint2(lo03[i], lo47[i]);
-      *reinterpret_cast<uint2*>(dst + (4 + i) * plane) = make_uint2(hi03[i], hi47[i]);
-    }
-  } else {
-    for (int e = 0; e < 8 && c + e < C; ++e)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) planes[i * plane + q * C + c + e] = (uint8_t)(v[e] >> (8 * i));
+  for (int i = 0; i < 4; ++i) {
+    *reinterpret_cast<uint2*>(dst + i * plane) = make_uint2(lo03[i], lo47[i]);
+    *reinterpret_cast<uint2*>(dst + (4 + i) * plane) = make_uint2(hi03[i], hi47[i]);
   }
 }
 
 // ------------------------------------------------------------------ implicit-GEMM conv
 
+constexpr int TKB = 64;                            // K bytes (channels) per pipeline stage = 2 MMA K steps
+constexpr int TPLANE = BM * TKB;                   // one limb tile per stage (8 KB)
 constexpr int EPI_WARPS = 16;                       // 4 per TMEM lane quarter, each a column group
 constexpr int PROD_WARP = EPI_WARPS, MMA_WARP = EPI_WARPS + 1;
 constexpr int TMA_THREADS = (EPI_WARPS + 2) * 32;  // + TMA producer warp + MMA issuer warp
-constexpr int TMA_MAX_STAGE = 4;
+constexpr int TMA_MAX_STAGE = 8;
 
+// Shift passes.  PASSES = 1: all 8 byte-shift accumulators of an NT <= 64 tile in TMEM at once.
+// PASSES = 2 (NT = 128): the high shifts 4..7 first (limbs max(0, 4-(J-1))..7), folded by the
+// epilogue into H = sum_{s>=4} acc_s 2^(8(s-4)) mod 2^32 (32 bits suffice: it is scaled by 2^32),
+// then the low shifts 0..3 (limbs 0..3) and y = sum_{s<4} acc_s 2^(8s) + 2^32 H.  Per output
+// column the limb tiles loaded drop from 8 (two NT = 64 tiles) to (J+3+4)/2 -- less L2->SM traffic,
+// which bounds this kernel (TMA ingress ~60 B/clk/SM at ~2400 clk L2 latency under load).
+template <int PASSES>
+struct Pass {
+  static constexpr int SPP = 8 / PASSES;                                          // shifts per pass
+  __host__ __device__ static constexpr int s_lo(int p) { return (PASSES - 1 - p) * SPP; }
+  __host__ __device__ static constexpr int l0(int p, int J) { return s_lo(p) - (J - 1) > 0 ? s_lo(p) - (J - 1) : 0; }
+  __host__ __device__ static constexpr int l1(int p) { return s_lo(p) + SPP - 1; }
+};
+
+// One pipeline stage's MMAs for pass P, everything but the stage base compile-time (the issue
+// rate of the single MMA thread matters: runtime loops around tcgen05.mma starve the tensor pipe).
+// Descriptors: adding (byte offset >> 4) to the start-address field of a base descriptor.
+template <int NT, int PASSES, int J, int P, bool FIRST>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t da0, uint64_t db0) {
+  using PS = Pass<PASSES>;
+  constexpr int SPP = PS::SPP, slo = PS::s_lo(P), shi = slo + SPP - 1, l0 = PS::l0(P, J), l1 = PS::l1(P);
+  constexpr int JMAX = 256 / NT;
+#pragma unroll
+  for (int ks = 0; ks < TKB / 32; ++ks) {
+#pragma unroll
+    for (int i = l0; i <= l1; ++i) {
+      const int j0 = slo - i > 0 ? slo - i : 0, j1 = shi - i < J - 1 ? shi - i : J - 1;
+      const uint64_t da = da0 + (uint64_t)(((i - l0) * TPLANE + ks * 32) >> 4);
+      if (FIRST && ks == 0) {
+        // first K step: one MMA per (i, j) so each shift accumulator starts with acc = 0
+#pragma unroll
+        for (int j = j0; j <= j1; ++j) {
+          const int sh = i + j, first_i = sh - (J - 1) > 0 ? sh - (J - 1) : 0;
+          mma_i8_w(tmem + (sh - slo) * NT, da, db0 + (uint64_t)((j * NT * TKB) >> 4), idesc_i8(NT),
+                 i == first_i ? 0u : 1u);
+        }
+      } else {
+        // weight limbs stacked along N: one MMA writes shifts i+jj .. i+jj+nj-1
+#pragma unroll
+        for (int jj = j0; jj <= j1; jj += JMAX) {
+          const int nj = j1 - jj + 1 < JMAX ? j1 - jj + 1 : JMAX;
+          mma_i8_w(tmem + (i + jj - slo) * NT, da, db0 + (uint64_t)((jj * NT * TKB + ks * 32) >> 4), idesc_i8(nj * NT),
+                 1u);
+        }
+      }
+    }
+  }
+}
+
+template <int NT, int PASSES, int J>
+__global__ void __launch_bounds__(TMA_THREADS, 1)
+    k_conv_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap8,
+               const TmaConvArgs A) {
+  using PS = Pass<PASSES>;
+  constexpr int SPP = PS::SPP;
+  constexpr int TMEM_COLS = SPP * NT < 32 ? 32 : SPP * NT;
+  static_assert(SPP * NT <= 512, "accumulators exceed TMEM");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // stage buffers 1024-aligned (SWIZZLE_64B atoms and TMA destinations)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_full[TMA_MAX_STAGE], bar_empty[TMA_MAX_STAGE], bar_tfull, bar_tempty;
+  __shared__ uint32_t tmem_base_s;
+
+  const int NS = A.nstage, nkb = A.nkb;
+  const int bbytes = J * NT * TKB;                  // weight tiles per stage
+  const int a_limbs = PASSES == 1 ? 8 : J + 3;      // most limb tiles any pass loads
+  const int stage_bytes = a_limbs * TPLANE + bbytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == MMA_WARP) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_empty[i], 1);
+    }
+    mbar_init(&bar_tfull, 1);
+    mbar_init(&bar_tempty, EPI_WARPS);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == PROD_WARP && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap8) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int S = A.OH * A.OW;
+
+  if (warp == PROD_WARP) {
+    // ================= TMA producer: per K block one TMA per limb tile of the pass + the weight tiles
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
+        const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+        const long long m0 = (long long)mt * BM;
+        const int b0 = (int)(m0 / S), rem = (int)(m0 - (long long)b0 * S);
+        const int oh0 = rem / A.OW, ow0 = rem - (rem / A.OW) * A.OW;
+        const int8_t* wsrc = A.wl + (long long)ntile * nkb * bbytes;
+        for (int p = 0; p < PASSES; ++p) {
+          const int l0 = PS::l0(p, J), nl = PS::l1(p) - l0 + 1;
+          const uint32_t tx = (uint32_t)(nl * TPLANE + bbytes);
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int st = it % NS;
+            if (it >= NS) mbar_wait(&bar_empty[st], ((it / NS) - 1) & 1);
+            const int tap = kb / A.ncc, cc = kb - tap * A.ncc;
+            const int ki = tap / A.kw, kj = tap - ki * A.kw;
+            uint8_t* sA = smem + st * stage_bytes;
+            if (A.dbg & 2) {  // profiling: no loads, MMAs on stale shared memory
+              mbar_arrive(&bar_full[st]);
+              continue;
+            }
+            mbar_expect_tx(&bar_full[st], tx);
+            const int w = ow0 * A.stride - A.pad + kj, h = oh0 * A.stride - A.pad + ki, bc = cc * A.B + b0;
+            if (nl == 8)  // all limbs in one box (tmap8: box limb extent 8)
+              tma_load_5d(sA, &tmap8, 0, w, h, bc, 0, &bar_full[st]);
+            else
+              for (int l = 0; l < nl; ++l) tma_load_5d(sA + l * TPLANE, &tmap, 0, w, h, bc, l0 + l, &bar_full[st]);
+            bulk_load(sA + a_limbs * TPLANE, wsrc + (long long)kb * bbytes, (uint32_t)bbytes, &bar_full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ================= MMA issuer
+    int it = 0, u = 0;  // u: (tile, pass) units, one TMEM fill each
+    long long c_te = 0, c_full = 0, c_issue = 0, c0;
+    const bool stamp = (A.dbg & 4) && A.stamps;
+    const long long cstart = clock64();
+    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
+#pragma unroll
+      for (int p = 0; p < PASSES; ++p, ++u) {
+        c0 = clock64();
+        if (u > 0) mbar_wait(&bar_tempty, (u - 1) & 1);  // epilogue drained the accumulators
+        tc_fence_after();
+        c_te += clock64() - c0;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int st = it % NS;
+          c0 = clock64();
+          mbar_wait(&bar_full[st], (it / NS) & 1);
+          tc_fence_after();
+          const long long c1 = clock64();
+          c_full += c1 - c0;
+          if (!(A.dbg & 1)) {  // whole warp, one elected lane issues (uniform operands)
+            const uint32_t aBase = smem_u32(smem + st * stage_bytes);
+            const uint64_t da0 = sdesc_k<TKB>(aBase), db0 = sdesc_k<TKB>(aBase + a_limbs * TPLANE);
+            if (p == 0) {
+              if (kb == 0)
+                issue_stage<NT, PASSES, J, 0, true>(tmem, da0, db0);
+              else
+                issue_stage<NT, PASSES, J, 0, false>(tmem, da0, db0);
+            } else {
+              if (kb == 0)
+                issue_stage<NT, PASSES, J, PASSES - 1, true>(tmem, da0, db0);
+              else
+                issue_stage<NT, PASSES, J, PASSES - 1, false>(tmem, da0, db0);
+            }
+          }
+          mma_commit_w(&bar_empty[st]);  // stage free once these MMAs complete
+          c_issue += clock64() - c1;
+        }
+        mma_commit_w(&bar_tfull);
+      }
+    }
+    if (stamp && lane == 0) {
+      long long* st = A.stamps + blockIdx.x * 8;
+      st[0] = clock64() - cstart;
+      st[1] = c_te;
+      st[2] = c_full;
+      st[3] = c_issue;
+      st[4] = it;
+      st[5] = u;
+    }
+  } else {
+    // ================= epilogue: warp w reads TMEM lane quarter w & 3 (tile rows [32q, 32q + 32)),
+    // column group w >> 2 (CPG of the NT columns, all shift accumulators of the pass)
+    constexpr int CPG = NT / 4 < 8 ? 8 : NT / 4;
+    constexpr int NGRP = NT / CPG;
+    constexpr int NCH = CPG / 8;
+    const int quarter = warp & 3, cgrp = warp >> 2;
+    int u = 0;
+    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
+      const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+      const long long em = (long long)mt * BM + quarter * 32 + lane;
+      const bool eok = em < A.M;
+      const int eb = eok ? (int)(em / S) : 0;
+      const long long esp = eok ? em - (long long)eb * S : 0;
+      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+      if constexpr (PASSES == 1) {
+        mbar_wait(&bar_tfull, u & 1);
+        ++u;
+        tc_fence_after();
+        if (cgrp < NGRP) {
+#pragma unroll 1
+          for (int c0 = cgrp * CPG; c0 < (cgrp + 1) * CPG; c0 += 8) {
+            uint32_t vv[8][8];
+#pragma unroll
+            for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
+            tmem_wait_ld();
+            u64 acc[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] = 0;
+#pragma unroll
+            for (int sh = 0; sh < 8; ++sh)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) acc[k] += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
+            if (c0 + 8 >= (cgrp + 1) * CPG) {  // this warp's accumulators drained
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&bar_tempty);
+            }
+            if (eok) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int n = ntile * NT + c0 + k;
+                if (n < A.N) {
+                  u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                  if (A.party == 0 && A.bias) yv += A.bias[n];
+                  A.y[((long long)eb * A.N + n) * S + esp] = yv;
+                }
+              }
+            }
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_tempty);
+        }
+        continue;
+      }
+      uint32_t hreg[NCH][8];  // PASSES == 2: high part H of each column (mod 2^32)
+#pragma unroll
+      for (int p = 0; p < PASSES; ++p, ++u) {
+        mbar_wait(&bar_tfull, u & 1);
+        tc_fence_after();
+        const bool last = p == PASSES - 1;
+        if (cgrp < NGRP) {
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const int c0 = cgrp * CPG + ch * 8;
+            uint32_t vv[SPP][8];
+#pragma unroll
+            for (int sh = 0; sh < SPP; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
+            tmem_wait_ld();
+            if (ch == NCH - 1) {  // this warp's accumulators drained: next pass / tile may start
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&bar_tempty);
+            }
+            u64 acc[8];
+            if (last) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                u64 a = PASSES == 2 ? (u64)hreg[ch][k] << 32 : 0ull;
+#pragma unroll
+                for (int sh = 0; sh < SPP; ++sh) a += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
+                acc[k] = a;
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                uint32_t h = 0;
+#pragma unroll
+                for (int sh = 0; sh < SPP; ++sh) h += vv[sh][k] << (8 * sh);  // mod 2^32
+                hreg[ch][k] = h;
+              }
+            }
+            if (!last) continue;
+            if (eok) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int n = ntile * NT + c0 + k;
+                if (n < A.N) {
+                  u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                  if (A.party == 0 && A.bias) yv += A.bias[n];
+                  A.y[((long long)eb * A.N + n) * S + esp] = yv;
+                }
+              }
+            }
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_tempty);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// ---- v1 (A/B reference for profiling; HB_TMA_V1=1)
 template <int NT>
 __global__ void __launch_bounds__(TMA_THREADS, 1)
-    k_conv_tma(const __grid_constant__ CUtensorMap tmap, const TmaConvArgs A) {
+    k_conv_tma_v1(const __grid_constant__ CUtensorMap tmap, const TmaConvArgs A) {
   constexpr int TMEM_COLS = 8 * NT < 32 ? 32 : 8 * NT;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // stage buffers 1024-aligned (SWIZZLE_64B atoms and TMA destinations)
@@ -157,6 +447,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
           const int tap = kb / A.ncc, cc = kb - tap * A.ncc;
           const int ki = tap / A.kw, kj = tap - ki * A.kw;
           uint8_t* sA = smem + st * stage_bytes;
+          if (A.dbg & 2) {
+            mbar_arrive(&bar_full[st]);
+            continue;
+          }
           mbar_expect_tx(&bar_full[st], tx_bytes);
           tma_load_5d(sA, &tmap, cc * KB, ow0 * A.stride - A.pad + kj, oh0 * A.stride - A.pad + ki, b0, 0,
                       &bar_full[st]);
@@ -324,6 +618,16 @@ int hb_tma_conv_box(int B, int OH, int OW, int* bb, int* bh, int* bw) {
   return 0;
 }
 
+long long* hb_tma_last_stamps = nullptr;
+
+extern "C" int hb_debug_tma_stamps(long long* host, long long cap) {
+  if (!hb_tma_last_stamps) return 0;
+  cudaDeviceSynchronize();
+  const long long n = cap < 1024 * 8 ? cap : 1024 * 8;
+  cudaMemcpy(host, hb_tma_last_stamps, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  return (int)n;
+}
+
 cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
                         const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias, uint64_t* y,
                         cudaStream_t s) {
@@ -342,7 +646,8 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   A.stride = stride;
   A.pad = pad;
   A.kw = kw;
-  A.ncc = C / KB;
+  A.ncc = C / TKB;
+  A.B = B;
   A.nkb = kh * kw * A.ncc;
   A.tiles_n = (N + nt - 1) / nt;
   A.tiles = (int)((A.M + BM - 1) / BM) * A.tiles_n;
@@ -356,39 +661,66 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
     return e ? atoi(e) : 0;
   }();
   A.dbg = dbg;
-  const int stage_bytes = 8 * PLANE + J * nt * KB;
+  const int passes = nt == 128 ? 2 : 1;
+  const int stage_bytes = (passes == 1 ? 8 : J + 3) * TPLANE + J * nt * TKB;
+  if (stage_bytes % 256) return cudaErrorInvalidValue;  // swizzle atoms stay aligned
   int ns = (227 * 1024 - 1024) / stage_bytes;
   A.nstage = ns > TMA_MAX_STAGE ? TMA_MAX_STAGE : ns;
   if (A.nstage < 2) return cudaErrorInvalidValue;
   const size_t smem = (size_t)A.nstage * stage_bytes + 1024;
 
-  // [limb][B][H][W][C] uint8, box (64 channels, bw*stride, bh*stride, bb, 8 limbs), traversal stride = conv stride
+  // planes [limb][C/64][B][H][W][64] uint8 as 5-D (64 channels, W, H, chunk*B + b, limb); box
+  // (64, bw*stride, bh*stride, bb, 1 limb), traversal stride = conv stride
   CUtensorMap tmap;
-  const cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, 8};
-  const cuuint64_t strides[4] = {(cuuint64_t)C, (cuuint64_t)W * C, (cuuint64_t)H * W * C,
+  const cuuint64_t dims[5] = {(cuuint64_t)TKB, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B * (C / TKB), 8};
+  const cuuint64_t strides[4] = {(cuuint64_t)TKB, (cuuint64_t)W * TKB, (cuuint64_t)H * W * TKB,
                                  (cuuint64_t)B * H * W * C};
-  const cuuint32_t box[5] = {(cuuint32_t)KB, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bb, 8};
+  const cuuint32_t box[5] = {(cuuint32_t)TKB, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bb, 1};
   const cuuint32_t estr[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
   if (box[1] > 256 || box[2] > 256) return cudaErrorInvalidValue;
   CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, TKB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (TKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  CUtensorMap tmap8;
+  const cuuint32_t box8[5] = {box[0], box[1], box[2], box[3], 8};
+  r = encode(&tmap8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes), dims, strides, box8, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             TKB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (TKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int grid = A.tiles < sm_count() ? A.tiles : sm_count();
   cudaError_t e;
-  switch (nt) {
-#define HB_NT(NT_)                                                                                      \
-  case NT_:                                                                                             \
-    e = cudaFuncSetAttribute(k_conv_tma<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                                     \
-    k_conv_tma<NT_><<<grid, TMA_THREADS, smem, s>>>(tmap, A);                                           \
-    break;
-    HB_NT(16)
-    HB_NT(32)
-    HB_NT(64)
-#undef HB_NT
-    default:
-      return cudaErrorInvalidValue;
+  static const bool v1 = getenv("HB_TMA_V1") != nullptr;
+  A.stamps = nullptr;
+  if (dbg & 4) {
+    static long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 1024 * 8 * sizeof(long long));
+    A.stamps = buf;
+    hb_tma_last_stamps = buf;
   }
-  return cudaGetLastError();
+  if (v1 && nt == 64) {
+    e = cudaFuncSetAttribute(k_conv_tma_v1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_conv_tma_v1<64><<<grid, TMA_THREADS, smem, s>>>(tmap8, A);
+    return cudaGetLastError();
+  }
+#define HB_NTJ(NT_, P_, J_)                                                                                     \
+  if (nt == NT_ && J == J_) {                                                                                    \
+    e = cudaFuncSetAttribute(k_conv_tma<NT_, P_, J_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                              \
+    k_conv_tma<NT_, P_, J_><<<grid, TMA_THREADS, smem, s>>>(tmap, tmap8, A);                                     \
+    return cudaGetLastError();                                                                                   \
+  }
+#define HB_NT(NT_, P_) HB_NTJ(NT_, P_, 1) HB_NTJ(NT_, P_, 2) HB_NTJ(NT_, P_, 3)
+  HB_NT(16, 1)
+  HB_NT(32, 1)
+  HB_NT(64, 1)
+  HB_NT(128, 2)
+#undef HB_NT
+#undef HB_NTJ
+  (void)e;
+  return cudaErrorInvalidValue;
 }
+

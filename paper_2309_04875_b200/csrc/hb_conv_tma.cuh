@@ -11,7 +11,7 @@ namespace tc {
 struct TmaConvArgs {
   long long M;         // output rows = B*OH*OW
   int N, J;            // output channels, weight limbs
-  int OH, OW, stride, pad, kw;
+  int B, OH, OW, stride, pad, kw;
   int ncc, nkb;        // 64-channel chunks, K blocks = kh*kw*ncc (order: tap-major, chunk-minor)
   int tiles_n, tiles;  // N tiles, total tiles (m-major, n-minor)
   const int8_t* wl;    // [N tiles][nkb][J][NT rows x 64 B, SWIZZLE_64B]
@@ -19,7 +19,8 @@ struct TmaConvArgs {
   const u64* bias;     // [N] (party 0) or null
   u64* y;              // NCHW [B][N][OH*OW]
   int nstage;          // smem pipeline depth
-  int dbg;             // HB_TC_DEBUG & 1: no MMAs (TMA throughput only)
+  int dbg;             // HB_TC_DEBUG & 1: no MMAs, & 2: no loads, & 4: MMA-warp clock stamps
+  long long* stamps;   // dbg & 4: per CTA [total, wait tmem-empty, wait full, issue, stages, units, -, -]
 };
 
 }  // namespace tc

@@ -17,6 +17,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // UMMA shared-memory descriptor, K-major, SWIZZLE_64B: rows of 64 bytes, 8-row atoms of 512 B
 // (SBO), 16-byte chunk index XOR (row >> 1) & 3 (cute Swizzle<2,4,3>); LBO unused for swizzled
 // K-major; version 1 (sm100); layout type 4 = SWIZZLE_64B (cute mma_sm100_desc.hpp).
+// Generic K-major swizzled descriptor: layout 6 = SWIZZLE_32B (SBO 256), 4 = SWIZZLE_64B (SBO 512),
+// 2 = SWIZZLE_128B (SBO 1024); SBO = 8 rows x row bytes.
+template <int ROWB>
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t addr) {
+  static_assert(ROWB == 32 || ROWB == 64 || ROWB == 128, "row bytes");
+  constexpr uint64_t layout = ROWB == 32 ? 6 : (ROWB == 64 ? 4 : 2);
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)((8 * ROWB) >> 4) << 32) | (1ull << 46) |
+         (layout << 61);
+}
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) |
          (4ull << 61);
@@ -33,6 +42,23 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+// Whole-warp variants: every lane executes the asm with warp-uniform operands (so they live in
+// uniform registers, no per-thread waterfall), one elected lane issues.
+__device__ __forceinline__ void mma_i8_w(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar)));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {

@@ -228,6 +228,7 @@ class _LimbWeight:
     kp_tc: int = 0
     nt: int = 0
     wl_tma: torch.Tensor | None = None  # int8 tiles for hb_conv_limbs_tma, K order (ki, kj, c)
+    nt_tma: int = 0                     # its N tile: 128 (two shift passes) when n >= 128
 
 
 def _balanced_limbs(w: np.ndarray):
@@ -268,30 +269,37 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
         lw.kp_tc = -(-k // 64) * 64
         lw.wl_tc = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt, lw.kp_tc)).to(dev)
         c = w.shape[1]
-        if c % 64 == 0:  # TMA path: 64-channel K blocks, tap-major K order
+        if c % TMA_KB == 0:  # TMA path: TMA_KB-channel K blocks, tap-major K order
             if w.ndim == 4:
                 kh, kw = w.shape[2], w.shape[3]
                 limbs_t = [l.reshape(n, c, kh, kw).transpose(0, 2, 3, 1).reshape(n, k) for l in limbs]
             else:
                 limbs_t = limbs
-            lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt, k)).to(dev)
+            lw.nt_tma = 128 if n >= 128 else lw.nt
+            lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt_tma, k, TMA_KB)).to(dev)
     return lw
 
 
-def _tc_tiles(limbs, n, k, nt, kp):
-    """Weight limbs in the tensor-core kernel's order [n tile][k block of 64][limb][row][64 B],
-    each [rows x 64 B] tile in the UMMA K-major SWIZZLE_64B layout: 16-byte chunk c of row r
-    stored at chunk c ^ ((r >> 1) & 3) (hb_ring_tc.cu canon())."""
+def _tc_tiles(limbs, n, k, nt, kp, kb=64):
+    """Weight limbs in a tensor-core kernel's order [n tile][k block of kb bytes][limb][row][kb B],
+    each [rows x kb B] tile in the UMMA K-major swizzled layout of that row width: 16-byte chunk c
+    of row r stored at chunk c ^ sw(r), sw = (r >> 1) & 3 (SWIZZLE_64B, hb_ring_tc.cu canon()) or
+    (r >> 2) & 1 (SWIZZLE_32B, hb_conv_tma.cu)."""
     j = len(limbs)
     ntiles = -(-n // nt)
     full = np.zeros((j, ntiles * nt, kp), dtype=np.int8)
     for jj, l in enumerate(limbs):
         full[jj, :n, :k] = l
-    t = full.reshape(j, ntiles, nt, kp // 64, 4, 16)                  # j, tile, row, kb, chunk, e
+    nch = kb // 16
+    t = full.reshape(j, ntiles, nt, kp // kb, nch, 16)                # j, tile, row, kb, chunk, e
     rows = np.arange(nt)
-    src_chunk = np.arange(4)[None, :] ^ ((rows[:, None] >> 1) & 3)  # stored chunk s holds chunk s ^ sw(r)
+    sw = (rows >> 1) & 3 if kb == 64 else (rows >> 2) & 1
+    src_chunk = np.arange(nch)[None, :] ^ sw[:, None]                  # stored chunk s holds chunk s ^ sw(r)
     t = t[:, :, rows[:, None], :, src_chunk, :]                       # -> (row, s, j, tile, kb, e)
     return np.ascontiguousarray(t.transpose(3, 4, 2, 0, 1, 5)).reshape(-1)  # tile, kb, j, row, s, e
+
+
+TMA_KB = 64  # channel bytes per stage of hb_conv_limbs_tma (hb_conv_tma.cu TKB)
 
 
 _WCACHE: dict = {}
@@ -359,7 +367,7 @@ def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int)
         s = _dev.stream_handle()
         planes = _limb_planes(x_nchw, s)
         _lib.call("hb_conv_limbs_tma", planes.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tma.data_ptr(),
-                  lw.n, lw.j, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
+                  lw.n, lw.j, lw.nt_tma, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
         return out
     _lib.call("hb_conv_limbs_tc", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
               lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(),

@@ -9,10 +9,13 @@ SHAPES = [  # (b, c, h, w, n, k, stride, pad)
     (512, 64, 32, 32, 64, 3, 1, 1), (512, 64, 32, 32, 128, 3, 2, 1), (512, 64, 32, 32, 128, 1, 2, 0),
     (512, 128, 16, 16, 128, 3, 1, 1), (512, 256, 8, 8, 256, 3, 1, 1), (512, 512, 4, 4, 512, 3, 1, 1),
     (512, 512, 1, 1, 10, 1, 1, 0), (3, 64, 5, 8, 20, 3, 1, 1), (130, 128, 4, 4, 70, 3, 1, 1),
+    (64, 128, 8, 8, 200, 3, 1, 1), (64, 64, 16, 16, 136, 3, 2, 1), (96, 256, 4, 4, 384, 3, 1, 1, 8.0),
+    (33, 192, 8, 8, 128, 1, 1, 0, 8.0),
 ]
 rng = np.random.default_rng(0)
-for (b, c, h, w, n, k, st, pad) in SHAPES:
-    W = rng.normal(0, np.sqrt(2 / (c * k * k)), (n, c, k, k)).astype(np.float32)
+for shp in SHAPES:
+    (b, c, h, w, n, k, st, pad), scale = shp[:8], (shp[8] if len(shp) > 8 else 1.0)
+    W = (scale * rng.normal(0, np.sqrt(2 / (c * k * k)), (n, c, k, k))).astype(np.float32)
     if k == 1 and h == 1:
         W = W.reshape(n, c)
     B = rng.normal(0, 0.1, n).astype(np.float32)

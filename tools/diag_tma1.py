@@ -13,3 +13,13 @@ for _ in range(3):
     nn._PLANES.clear()
     nn._gemm_tc(x, (k, k, st, pad), lw, 0, 16)
 torch.cuda.synchronize()
+import os
+if int(os.environ.get("HB_TC_DEBUG", "0")) & 4:
+    import ctypes
+    from paper_2309_04875_b200 import _lib
+    lib = _lib.load()
+    lib.hb_debug_tma_stamps.restype = ctypes.c_int
+    buf = np.zeros(1024 * 8, dtype=np.int64)
+    lib.hb_debug_tma_stamps(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), buf.size)
+    st = buf.reshape(-1, 8)[:148]
+    print("MMA warp per CTA (mean clk): total %.0f  wait tmem-empty %.0f  wait full %.0f  issue %.0f  stages %.0f units %.0f" % tuple(st[:, :6].mean(0)))
