@@ -189,10 +189,11 @@ int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int wi
  * hb_conv_limbs_tc.  wlimbs: int8 [ceil(n_out/n_tile)][kh*kw*channels/64][j_limbs][n_tile x 64
  * SWIZZLE_64B K-major tile], K order (ki, kj, c), n_tile in {16, 32, 64, 128} (128: two shift
  * passes).  channels % 64 == 0; the output (OH, OW) must tile
- * into 128-pixel (batch, oh, ow) boxes (OW a divisor or multiple of 128, ...). */
+ * into 128-pixel (batch, oh, ow) boxes (OW a divisor or multiple of 128, ...).  residual: optional NCHW
+ * share of y's shape added after truncation and bias (a ResNet block's add_shares, sharing.py:118-122). */
 int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
                       int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
-                      int frac_bits, const uint64_t* bias, uint64_t* y, void* stream);
+                      int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream);
 
 #ifdef __cplusplus
 }

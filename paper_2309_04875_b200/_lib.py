@@ -94,7 +94,7 @@ _SIGS = {
                                                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p,
                                                                         u64p, ctypes.c_void_p]),
     "hb_limbs_nhwc": (ctypes.c_int, [u64p] + [ctypes.c_int] * 4 + [u64p, ctypes.c_void_p]),
-    "hb_conv_limbs_tma": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p] + [ctypes.c_int] * 5 + [u64p, u64p,
+    "hb_conv_limbs_tma": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p] + [ctypes.c_int] * 5 + [u64p, u64p, u64p,
                                                                                                  ctypes.c_void_p]),
 }
 

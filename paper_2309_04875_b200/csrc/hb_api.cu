@@ -469,7 +469,7 @@ int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int wi
 
 int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
                       int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
-                      int frac_bits, const uint64_t* bias, uint64_t* y, void* stream) {
+                      int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream) {
   if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
     return fail(HB_ERR_CONFIG, "bad conv geometry");
   if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
@@ -486,7 +486,7 @@ int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height
   if (hb_tma_conv_box(batch, oh, ow, &bb, &bh, &bw))
     return fail(HB_ERR_CONFIG, "output %dx%d does not tile into 128-pixel boxes", oh, ow);
   return cuda_status(hb_tma_conv(planes, batch, channels, height, width, kh, kw, stride, pad, wlimbs, n_out, j_limbs,
-                                 n_tile, party, frac_bits, bias, y, S(stream)),
+                                 n_tile, party, frac_bits, bias, residual, y, S(stream)),
                      "hb_conv_limbs_tma");
 }
 

@@ -159,12 +159,17 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                const TmaConvArgs A) {
   using PS = Pass<PASSES>;
   constexpr int SPP = PS::SPP;
-  constexpr int TMEM_COLS = SPP * NT < 32 ? 32 : SPP * NT;
-  static_assert(SPP * NT <= 512, "accumulators exceed TMEM");
+  // DB: two accumulator buffers when a pass fits in half of TMEM -- pass p of every tile uses
+  // buffer p, so the epilogue of one pass overlaps the MMAs of the next
+  constexpr bool DB = PASSES == 2 && 2 * SPP * NT <= 512;
+  constexpr int NB = DB ? 2 : 1;
+  constexpr int UCOLS = SPP * NT;  // TMEM columns of one unit (tile pass)
+  constexpr int TMEM_COLS = NB * UCOLS < 32 ? 32 : NB * UCOLS;
+  static_assert(UCOLS <= 512, "accumulators exceed TMEM");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // stage buffers 1024-aligned (SWIZZLE_64B atoms and TMA destinations)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_full[TMA_MAX_STAGE], bar_empty[TMA_MAX_STAGE], bar_tfull, bar_tempty;
+  __shared__ uint64_t bar_full[TMA_MAX_STAGE], bar_empty[TMA_MAX_STAGE], bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_s;
 
   const int NS = A.nstage, nkb = A.nkb;
@@ -179,8 +184,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
       mbar_init(&bar_full[i], 1);
       mbar_init(&bar_empty[i], 1);
     }
-    mbar_init(&bar_tfull, 1);
-    mbar_init(&bar_tempty, EPI_WARPS);  // one arrival per epilogue warp
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_tfull[b], 1);
+      mbar_init(&bar_tempty[b], EPI_WARPS);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == PROD_WARP && lane == 0) {
@@ -236,8 +243,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
 #pragma unroll
       for (int p = 0; p < PASSES; ++p, ++u) {
+        const int buf = DB ? (u & 1) : 0;
+        const uint32_t tm = tmem + buf * UCOLS;
         c0 = clock64();
-        if (u > 0) mbar_wait(&bar_tempty, (u - 1) & 1);  // epilogue drained the accumulators
+        if (u >= NB) mbar_wait(&bar_tempty[buf], ((u / NB) - 1) & 1);  // epilogue drained this buffer
         tc_fence_after();
         c_te += clock64() - c0;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -252,20 +261,20 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             const uint64_t da0 = sdesc_k<TKB>(aBase), db0 = sdesc_k<TKB>(aBase + a_limbs * TPLANE);
             if (p == 0) {
               if (kb == 0)
-                issue_stage<NT, PASSES, J, 0, true>(tmem, da0, db0);
+                issue_stage<NT, PASSES, J, 0, true>(tm, da0, db0);
               else
-                issue_stage<NT, PASSES, J, 0, false>(tmem, da0, db0);
+                issue_stage<NT, PASSES, J, 0, false>(tm, da0, db0);
             } else {
               if (kb == 0)
-                issue_stage<NT, PASSES, J, PASSES - 1, true>(tmem, da0, db0);
+                issue_stage<NT, PASSES, J, PASSES - 1, true>(tm, da0, db0);
               else
-                issue_stage<NT, PASSES, J, PASSES - 1, false>(tmem, da0, db0);
+                issue_stage<NT, PASSES, J, PASSES - 1, false>(tm, da0, db0);
             }
           }
           mma_commit_w(&bar_empty[st]);  // stage free once these MMAs complete
           c_issue += clock64() - c1;
         }
-        mma_commit_w(&bar_tfull);
+        mma_commit_w(&bar_tfull[buf]);
       }
     }
     if (stamp && lane == 0) {
@@ -292,8 +301,12 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
       const int eb = eok ? (int)(em / S) : 0;
       const long long esp = eok ? em - (long long)eb * S : 0;
       const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+      if (A.res && eok && cgrp < NGRP)  // residual lines into L2 while the MMAs run
+        for (int c = cgrp * CPG; c < (cgrp + 1) * CPG; ++c)
+          if (ntile * NT + c < A.N)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(A.res + ((long long)eb * A.N + ntile * NT + c) * S + esp));
       if constexpr (PASSES == 1) {
-        mbar_wait(&bar_tfull, u & 1);
+        mbar_wait(&bar_tfull[0], u & 1);
         ++u;
         tc_fence_after();
         if (cgrp < NGRP) {
@@ -302,10 +315,21 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             uint32_t vv[8][8];
 #pragma unroll
             for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
-            tmem_wait_ld();
             u64 acc[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] = 0;
+            for (int k = 0; k < 8; ++k) {  // residual loads overlap the TMEM loads
+              const int n = ntile * NT + c0 + k;
+              acc[k] = (A.res && eok && n < A.N) ? __ldg(reinterpret_cast<const unsigned long long*>(
+                                                        A.res + ((long long)eb * A.N + n) * S + esp))
+                                                  : 0ull;
+            }
+            tmem_wait_ld();
+            u64 rsd[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              rsd[k] = acc[k];
+              acc[k] = 0;
+            }
 #pragma unroll
             for (int sh = 0; sh < 8; ++sh)
 #pragma unroll
@@ -313,7 +337,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             if (c0 + 8 >= (cgrp + 1) * CPG) {  // this warp's accumulators drained
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&bar_tempty);
+              if (lane == 0) mbar_arrive(&bar_tempty[0]);
             }
             if (eok) {
 #pragma unroll
@@ -322,6 +346,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                 if (n < A.N) {
                   u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
                   if (A.party == 0 && A.bias) yv += A.bias[n];
+                  yv += rsd[k];  // fused residual add (add_shares, sharing.py:118-122); 0 without one
                   A.y[((long long)eb * A.N + n) * S + esp] = yv;
                 }
               }
@@ -330,28 +355,30 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         } else {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_tempty);
+          if (lane == 0) mbar_arrive(&bar_tempty[0]);
         }
         continue;
       }
       uint32_t hreg[NCH][8];  // PASSES == 2: high part H of each column (mod 2^32)
 #pragma unroll
       for (int p = 0; p < PASSES; ++p, ++u) {
-        mbar_wait(&bar_tfull, u & 1);
+        const int buf = DB ? (u & 1) : 0;
+        mbar_wait(&bar_tfull[buf], (u / NB) & 1);
         tc_fence_after();
         const bool last = p == PASSES - 1;
+        const uint32_t ubase = lane_base + buf * UCOLS;
         if (cgrp < NGRP) {
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) {
             const int c0 = cgrp * CPG + ch * 8;
             uint32_t vv[SPP][8];
 #pragma unroll
-            for (int sh = 0; sh < SPP; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
+            for (int sh = 0; sh < SPP; ++sh) tmem_ld8(ubase + sh * NT + c0, vv[sh]);
             tmem_wait_ld();
             if (ch == NCH - 1) {  // this warp's accumulators drained: next pass / tile may start
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&bar_tempty);
+              if (lane == 0) mbar_arrive(&bar_tempty[buf]);
             }
             u64 acc[8];
             if (last) {
@@ -379,7 +406,9 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                 if (n < A.N) {
                   u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
                   if (A.party == 0 && A.bias) yv += A.bias[n];
-                  A.y[((long long)eb * A.N + n) * S + esp] = yv;
+                  const long long oi = ((long long)eb * A.N + n) * S + esp;
+                  if (A.res) yv += __ldg(reinterpret_cast<const unsigned long long*>(A.res + oi));  // add_shares
+                  A.y[oi] = yv;
                 }
               }
             }
@@ -387,168 +416,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         } else {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_tempty);
+          if (lane == 0) mbar_arrive(&bar_tempty[buf]);
         }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == MMA_WARP) tmem_dealloc<TMEM_COLS>(tmem);
-}
-
-// ---- v1 (A/B reference for profiling; HB_TMA_V1=1)
-template <int NT>
-__global__ void __launch_bounds__(TMA_THREADS, 1)
-    k_conv_tma_v1(const __grid_constant__ CUtensorMap tmap, const TmaConvArgs A) {
-  constexpr int TMEM_COLS = 8 * NT < 32 ? 32 : 8 * NT;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // stage buffers 1024-aligned (SWIZZLE_64B atoms and TMA destinations)
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_full[TMA_MAX_STAGE], bar_empty[TMA_MAX_STAGE], bar_tfull, bar_tempty;
-  __shared__ uint32_t tmem_base_s;
-
-  const int J = A.J, NS = A.nstage, nkb = A.nkb;
-  const int bbytes = J * NT * KB;                 // weight tiles per stage
-  const int stage_bytes = 8 * PLANE + bbytes;     // multiple of 1024
-  const uint32_t tx_bytes = (uint32_t)stage_bytes;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (warp == MMA_WARP) tmem_alloc<TMEM_COLS>(&tmem_base_s);
-  if (tid == 0) {
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&bar_full[i], 1);
-      mbar_init(&bar_empty[i], 1);
-    }
-    mbar_init(&bar_tfull, 1);
-    mbar_init(&bar_tempty, EPI_WARPS);  // one arrival per epilogue warp
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == PROD_WARP && lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_s;
-  const int S = A.OH * A.OW;
-
-  if (warp == PROD_WARP) {
-    // ================= TMA producer
-    if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
-        const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
-        const long long m0 = (long long)mt * BM;
-        const int b0 = (int)(m0 / S), rem = (int)(m0 - (long long)b0 * S);
-        const int oh0 = rem / A.OW, ow0 = rem - (rem / A.OW) * A.OW;
-        const int8_t* wsrc = A.wl + (long long)ntile * nkb * bbytes;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int st = it % NS;
-          if (it >= NS) mbar_wait(&bar_empty[st], ((it / NS) - 1) & 1);
-          const int tap = kb / A.ncc, cc = kb - tap * A.ncc;
-          const int ki = tap / A.kw, kj = tap - ki * A.kw;
-          uint8_t* sA = smem + st * stage_bytes;
-          if (A.dbg & 2) {
-            mbar_arrive(&bar_full[st]);
-            continue;
-          }
-          mbar_expect_tx(&bar_full[st], tx_bytes);
-          tma_load_5d(sA, &tmap, cc * KB, ow0 * A.stride - A.pad + kj, oh0 * A.stride - A.pad + ki, b0, 0,
-                      &bar_full[st]);
-          bulk_load(sA + 8 * PLANE, wsrc + (long long)kb * bbytes, (uint32_t)bbytes, &bar_full[st]);
-        }
-      }
-    }
-  } else if (warp == MMA_WARP) {
-    // ================= MMA issuer
-    int it = 0, lt = 0;
-    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
-      if (lt > 0) mbar_wait(&bar_tempty, (lt - 1) & 1);  // epilogue drained the accumulators
-      tc_fence_after();
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int st = it % NS;
-        mbar_wait(&bar_full[st], (it / NS) & 1);
-        tc_fence_after();
-        if (lane == 0 && !(A.dbg & 1)) {
-          const uint32_t aBase = smem_u32(smem + st * stage_bytes), bBase = aBase + 8 * PLANE;
-#pragma unroll
-          for (int ks = 0; ks < KB / 32; ++ks) {
-            if (kb == 0 && ks == 0) {
-              // first K step: one MMA per (i, j) so every shift accumulator starts with acc = 0
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                for (int j = 0; j < J && i + j < 8; ++j) {
-                  const int sh = i + j, first_i = sh - (J - 1) > 0 ? sh - (J - 1) : 0;
-                  mma_i8(tmem + sh * NT, sdesc(aBase + i * PLANE), sdesc(bBase + j * NT * KB), idesc_i8(NT),
-                         i == first_i ? 0u : 1u);
-                }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int nj = J < 8 - i ? J : 8 - i;
-                mma_i8(tmem + i * NT, sdesc(aBase + i * PLANE + ks * 32), sdesc(bBase + ks * 32), idesc_i8(nj * NT),
-                       1u);
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mma_commit(&bar_empty[st]);  // stage free once these MMAs complete
-        __syncwarp();
-      }
-      if (lane == 0) mma_commit(&bar_tfull);
-      __syncwarp();
-    }
-  } else {
-    // ================= epilogue: warp w reads TMEM lane quarter w & 3 (tile rows [32q, 32q + 32)),
-    // column group w >> 2 (CPG of the NT columns, all 8 shift accumulators)
-    constexpr int CPG = NT / 4 < 8 ? 8 : NT / 4;
-    constexpr int NGRP = NT / CPG;
-    const int quarter = warp & 3, cgrp = warp >> 2;
-    int lt = 0;
-    for (int t = blockIdx.x; t < A.tiles; t += gridDim.x, ++lt) {
-      const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
-      const long long em = (long long)mt * BM + quarter * 32 + lane;
-      const bool eok = em < A.M;
-      const int eb = eok ? (int)(em / S) : 0;
-      const long long esp = eok ? em - (long long)eb * S : 0;
-      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-      mbar_wait(&bar_tfull, lt & 1);
-      tc_fence_after();
-      if (cgrp < NGRP) {
-#pragma unroll 1
-        for (int c0 = cgrp * CPG; c0 < (cgrp + 1) * CPG; c0 += 8) {
-          uint32_t vv[8][8];
-#pragma unroll
-          for (int sh = 0; sh < 8; ++sh) tmem_ld8(lane_base + sh * NT + c0, vv[sh]);
-          tmem_wait_ld();
-          u64 acc[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] = 0;
-#pragma unroll
-          for (int sh = 0; sh < 8; ++sh)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] += (u64)(long long)(int32_t)vv[sh][k] << (8 * sh);
-          if (c0 + 8 >= (cgrp + 1) * CPG) {  // this warp's accumulators drained
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_tempty);
-          }
-          if (eok) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int n = ntile * NT + c0 + k;
-              if (n < A.N) {
-                u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
-                if (A.party == 0 && A.bias) yv += A.bias[n];
-                A.y[((long long)eb * A.N + n) * S + esp] = yv;
-              }
-            }
-          }
-        }
-      } else {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_tempty);
       }
     }
   }
@@ -629,8 +498,8 @@ extern "C" int hb_debug_tma_stamps(long long* host, long long cap) {
 }
 
 cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
-                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias, uint64_t* y,
-                        cudaStream_t s) {
+                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias,
+                        const uint64_t* res, uint64_t* y, cudaStream_t s) {
   using namespace hb::tc;
   auto encode = encode_fn();
   if (!encode) return cudaErrorNotSupported;
@@ -655,13 +524,18 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   A.party = party;
   A.frac = frac;
   A.bias = bias;
+  A.res = res;
   A.y = y;
   static const int dbg = [] {
     const char* e = getenv("HB_TC_DEBUG");
     return e ? atoi(e) : 0;
   }();
   A.dbg = dbg;
-  const int passes = nt == 128 ? 2 : 1;
+  static const bool p2d = [] {  // double-buffered two-pass NT=64 (measured slower; experiments only)
+    const char* e = getenv("HB_TMA_P2D");
+    return e && atoi(e);
+  }();
+  const int passes = nt == 128 || (nt == 64 && p2d) ? 2 : 1;
   const int stage_bytes = (passes == 1 ? 8 : J + 3) * TPLANE + J * nt * TKB;
   if (stage_bytes % 256) return cudaErrorInvalidValue;  // swizzle atoms stay aligned
   int ns = (227 * 1024 - 1024) / stage_bytes;
@@ -692,20 +566,6 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int grid = A.tiles < sm_count() ? A.tiles : sm_count();
   cudaError_t e;
-  static const bool v1 = getenv("HB_TMA_V1") != nullptr;
-  A.stamps = nullptr;
-  if (dbg & 4) {
-    static long long* buf = nullptr;
-    if (!buf) cudaMalloc(&buf, 1024 * 8 * sizeof(long long));
-    A.stamps = buf;
-    hb_tma_last_stamps = buf;
-  }
-  if (v1 && nt == 64) {
-    e = cudaFuncSetAttribute(k_conv_tma_v1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_conv_tma_v1<64><<<grid, TMA_THREADS, smem, s>>>(tmap8, A);
-    return cudaGetLastError();
-  }
 #define HB_NTJ(NT_, P_, J_)                                                                                     \
   if (nt == NT_ && J == J_) {                                                                                    \
     e = cudaFuncSetAttribute(k_conv_tma<NT_, P_, J_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -716,6 +576,9 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
 #define HB_NT(NT_, P_) HB_NTJ(NT_, P_, 1) HB_NTJ(NT_, P_, 2) HB_NTJ(NT_, P_, 3)
   HB_NT(16, 1)
   HB_NT(32, 1)
+  if (passes == 2) {
+    HB_NT(64, 2)
+  }
   HB_NT(64, 1)
   HB_NT(128, 2)
 #undef HB_NT

@@ -17,6 +17,7 @@ struct TmaConvArgs {
   const int8_t* wl;    // [N tiles][nkb][J][NT rows x 64 B, SWIZZLE_64B]
   int party, frac;
   const u64* bias;     // [N] (party 0) or null
+  const u64* res;      // NCHW [B][N][OH*OW] residual share added to y, or null
   u64* y;              // NCHW [B][N][OH*OW]
   int nstage;          // smem pipeline depth
   int dbg;             // HB_TC_DEBUG & 1: no MMAs, & 2: no loads, & 4: MMA-warp clock stamps
@@ -30,5 +31,5 @@ cudaError_t hb_limbs_nhwc_launch(const uint64_t* x, long long B, int C, long lon
                                  cudaStream_t s);
 int hb_tma_conv_box(int B, int OH, int OW, int* bb, int* bh, int* bw);
 cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
-                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias, uint64_t* y,
-                        cudaStream_t s);
+                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias,
+                        const uint64_t* res, uint64_t* y, cudaStream_t s);

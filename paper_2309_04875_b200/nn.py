@@ -275,7 +275,7 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
                 limbs_t = [l.reshape(n, c, kh, kw).transpose(0, 2, 3, 1).reshape(n, k) for l in limbs]
             else:
                 limbs_t = limbs
-            lw.nt_tma = 128 if n >= 128 else lw.nt
+            lw.nt_tma = 128 if n >= 128 and _TMA_WIDE else lw.nt
             lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt_tma, k, TMA_KB)).to(dev)
     return lw
 
@@ -300,6 +300,7 @@ def _tc_tiles(limbs, n, k, nt, kp, kb=64):
 
 
 TMA_KB = 64  # channel bytes per stage of hb_conv_limbs_tma (hb_conv_tma.cu TKB)
+_TMA_WIDE = os.environ.get("HB_TMA_NT", "128") != "64"  # N tile 128 (two passes) for n >= 128
 
 
 _WCACHE: dict = {}
@@ -355,7 +356,15 @@ def _tma_box_ok(oh: int, ow: int) -> bool:
     return oh % rows == 0 if oh >= rows else rows % oh == 0
 
 
-def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int) -> torch.Tensor:
+def _tma_ok(x_nchw: torch.Tensor, geom, lw: _LimbWeight) -> bool:
+    b, c, h, w = x_nchw.shape
+    kh, kw, stride, pad = geom
+    oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    return RING_GEMM == "tc" and lw.wl_tma is not None and stride <= 8 and b > 0 and _tma_box_ok(oh, ow)
+
+
+def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int,
+             residual: torch.Tensor | None = None) -> torch.Tensor:
     """tcgen05 ring conv: NCHW share in, NCHW [b, n, oh, ow] share out.  TMA-fed implicit GEMM over
     NHWC limb planes (hb_limbs_nhwc + hb_conv_limbs_tma) when the layer qualifies, else the fused
     gather kernel (hb_conv_limbs_tc)."""
@@ -363,12 +372,17 @@ def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int)
     kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
     out = torch.empty((b, lw.n, oh, ow), dtype=torch.int64, device=x_nchw.device)
-    if RING_GEMM == "tc" and lw.wl_tma is not None and stride <= 8 and _tma_box_ok(oh, ow) and b > 0:
+    if _tma_ok(x_nchw, geom, lw):
         s = _dev.stream_handle()
         planes = _limb_planes(x_nchw, s)
+        if residual is not None and residual.shape != out.shape:
+            raise ConfigError(f"residual shape {tuple(residual.shape)} != conv output {tuple(out.shape)}")
         _lib.call("hb_conv_limbs_tma", planes.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tma.data_ptr(),
-                  lw.n, lw.j, lw.nt_tma, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(), s)
+                  lw.n, lw.j, lw.nt_tma, party, frac, lw.bias.data_ptr() if party == 0 else None,
+                  None if residual is None else residual.contiguous().data_ptr(), out.data_ptr(), s)
         return out
+    if residual is not None:
+        raise ConfigError("residual fusion needs the TMA conv path")
     _lib.call("hb_conv_limbs_tc", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tc.data_ptr(), lw.n, lw.j,
               lw.kp_tc, lw.nt, party, frac, lw.bias.data_ptr() if party == 0 else None, out.data_ptr(),
               _dev.stream_handle())
@@ -402,12 +416,13 @@ def _to_layout(d: torch.Tensor, have: str, want: str) -> torch.Tensor:
     return d.permute(0, 3, 1, 2).contiguous()
 
 
-def _conv_dev(d, lay, L: Conv2d, lw, party, frac):
-    """Conv on a device share in layout `lay`; returns (output, its layout)."""
+def _conv_dev(d, lay, L: Conv2d, lw, party, frac, residual=None):
+    """Conv on a device share in layout `lay`; returns (output, its layout).  `residual` (NCHW, the
+    output's shape) is added in the TMA kernel's epilogue (callers check _conv_fusable first)."""
     geom = (L.kh, L.kw, L.stride, L.pad)
     d = _to_layout(d, lay, "nchw")
     if _use_tc(lw):
-        return _gemm_tc(d, geom, lw, party, frac), "nchw"
+        return _gemm_tc(d, geom, lw, party, frac, residual), "nchw"
     return _gemm_cublaslt(d, geom, lw, party, frac, 1), "nchw"
 
 
@@ -495,6 +510,16 @@ def _add_dev(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def _has_relu(layers) -> bool:
+    return any(isinstance(L, Relu) or (isinstance(L, Residual) and (_has_relu(L.body) or _has_relu(L.shortcut)))
+               for L in layers)
+
+
+def _conv_out_shape(d: torch.Tensor, L: Conv2d):
+    b, _, h, w = d.shape
+    return torch.Size((b, L.out_channels, (h + 2 * L.pad - L.kh) // L.stride + 1, (w + 2 * L.pad - L.kw) // L.stride + 1))
+
+
 def _meter_delta(ep, before):
     after = ep.meter.snapshot()
     return sum(after[t][0] - before[t][0] for t in after), sum(after[t][1] - before[t][1] for t in after)
@@ -523,10 +548,29 @@ def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_me
                         out = [protocol.relu(sessions[0], shares[0], win)]
                     ds = [o.data for o in out]
             elif isinstance(L, Residual):
-                a, la = run(L.body, ds, lay, f"{prefix}{i}.body.")
-                h, lh = run(L.shortcut, ds, lay, f"{prefix}{i}.short.")
-                ds = [_add_dev(x, _to_layout(y, lh, la)) for x, y in zip(a, h)]
-                lay = la
+                last = L.body[-1] if L.body else None
+                if (layer_meter is None and isinstance(last, Conv2d) and RING_GEMM == "tc"
+                        and not _has_relu(L.shortcut)):
+                    # shortcut first (no ReLU: it opens nothing and draws no triples, so triple order
+                    # and meters are unchanged), then the body with add_shares fused into its last conv
+                    h, lh = run(L.shortcut, ds, lay, f"{prefix}{i}.short.")
+                    a, la = run(L.body[:-1], ds, lay, f"{prefix}{i}.body.")
+                    a = [_to_layout(d, la, "nchw") for d in a]
+                    h = [_to_layout(y, lh, "nchw") for y in h]
+                    lw = _weight(model.weights[last.weight], model.weights[last.bias], cfg)
+                    geom = (last.kh, last.kw, last.stride, last.pad)
+                    if _use_tc(lw) and _tma_ok(a[0], geom, lw) and all(
+                            y.shape == _conv_out_shape(d, last) for d, y in zip(a, h)):
+                        ds = [_conv_dev(d, "nchw", last, lw, p, cfg.frac_bits, y)[0] for d, p, y in zip(a, parties, h)]
+                    else:
+                        ds = [_add_dev(_conv_dev(d, "nchw", last, lw, p, cfg.frac_bits)[0], y)
+                              for d, p, y in zip(a, parties, h)]
+                    lay = "nchw"
+                else:
+                    a, la = run(L.body, ds, lay, f"{prefix}{i}.body.")
+                    h, lh = run(L.shortcut, ds, lay, f"{prefix}{i}.short.")
+                    ds = [_add_dev(x, _to_layout(y, lh, la)) for x, y in zip(a, h)]
+                    lay = la
             elif isinstance(L, Conv2d):
                 lw = _weight(model.weights[L.weight], model.weights[L.bias], cfg)
                 res = [_conv_dev(d, lay, L, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]
