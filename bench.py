@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--triple-gb", type=float, default=64.0, help="HBM budget for stocked triples")
     p.add_argument("--workload", choices=["relu", "resnet18", "resnet50"], default="relu")
     p.add_argument("--batch", type=int, default=None, help="ResNet batch (default 512 / 128)")
+    p.add_argument("--resnet-triple-gb", type=float, default=100.0,
+                   help="HBM budget for one ResNet micro-batch's triples (both parties)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                    help="N>1 exchange backend (gloo lets 2 ranks share one GPU for testing)")
     return p.parse_args()
@@ -329,7 +331,20 @@ def run_resnet(args):
         model, batch, shape = models.resnet50(0), args.batch or 128, (3, 64, 64)
     win = BitWindow(args.k, args.m)
     cfg = models.resnet_relu_config(model, win)
-    need = nn.triple_requirements(model, cfg, batch)
+
+    def triple_bytes(b):  # both parties' (a, b, c) streams for a forward of b samples
+        return sum(3 * 2 * (-(-c * w // 64) * 8 if kind == "bool" else 8 * c)
+                   for (kind, w), c in nn.triple_requirements(model, cfg, b).items())
+
+    # micro-batches when the whole batch's triples exceed the HBM budget (ResNet50 b128 at 64x64
+    # needs ~208 GB); each micro-batch forward reads its full triple stock from HBM, and the stock
+    # is rewound between micro-batches and steps (the dealer is the offline phase, not timed)
+    mb = batch
+    while mb > 1 and triple_bytes(mb) > args.resnet_triple_gb * 2**30:
+        mb //= 2
+    if batch % mb:
+        raise SystemExit(f"batch {batch} does not split into micro-batches of {mb}")
+    need = nn.triple_requirements(model, cfg, mb)
     eps = transport.local_pair()
     stores = (dealer.TripleStore(0), dealer.TripleStore(1))
     for i, ((kind, width), count) in enumerate(sorted(need.items())):
@@ -340,14 +355,18 @@ def run_resnet(args):
     x_f = torch.rand((batch,) + shape, generator=g, device=dev, dtype=torch.float64)
     enc = torch.floor(x_f * 65536.0 + 0.5).to(torch.int64)
     r = torch.empty_like(enc).random_(generator=g)
-    x0, x1 = ArithShareTensor(0, 64, enc + r), ArithShareTensor(1, 64, -r)
+    x0s = [ArithShareTensor(0, 64, (enc + r)[i:i + mb]) for i in range(0, batch, mb)]
+    x1s = [ArithShareTensor(1, 64, (-r)[i:i + mb]) for i in range(0, batch, mb)]
     s = torch.cuda.current_stream()
 
     def fwd():
-        for st in stores:
-            for (kind, width) in need:
-                st.rewind(kind, width)
-        return nn.model_forward_pair(sessions, x0, x1, model, cfg)
+        out = None
+        for x0, x1 in zip(x0s, x1s):
+            for st in stores:
+                for (kind, width) in need:
+                    st.rewind(kind, width)
+            out = nn.model_forward_pair(sessions, x0, x1, model, cfg)
+        return out
 
     for _ in range(args.warmup):
         y0, y1 = fwd()
@@ -370,6 +389,7 @@ def run_resnet(args):
         "config": {"workload": f"{args.workload} private inference, batch {batch}, input {shape}, "
                                f"all ReLU groups window ({args.k},{args.m})", "batch": batch,
                    "relu_elements_per_forward": relu_elems, "parties": "1 pair time-sliced on 1 GPU",
+                   "micro_batch": mb, "stem": "CIFAR-style 3x3 stride 1, no maxpool",
                    "path": "nn.model_forward_pair: int8-limb ring conv ("
                            + ("hand-written tcgen05 kernel" if nn.RING_GEMM == "tc" else "cuBLASLt") + ") + fused pair ReLU kernel",
                    "weights": "random init (torchvision scheme), BN folded", "parallelism": "pair"},
