@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     constexpr int NCH = CPG / 8;
     const int quarter = warp & 3, cgrp = warp >> 2;
     int u = 0;
+    long long e_wait = 0, e_read = 0, e_a = 0;  // dbg & 4 (warp 0): tfull waits, tfull -> tempty-arrive
     for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
       const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
       const long long em = (long long)mt * BM + quarter * 32 + lane;
@@ -306,10 +307,47 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
           if (ntile * NT + c < A.N)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(A.res + ((long long)eb * A.N + ntile * NT + c) * S + esp));
       if constexpr (PASSES == 1) {
+        e_a = clock64();
         mbar_wait(&bar_tfull[0], u & 1);
         ++u;
         tc_fence_after();
-        if (cgrp < NGRP) {
+        {
+          const long long e_b = clock64();
+          e_wait += e_b - e_a;
+          e_a = e_b;
+        }
+        if (cgrp < NGRP && CPG == 16) {
+          // 16 columns x 8 shifts per thread: one 16-column TMEM load per shift, folded as it lands
+          const int cb = cgrp * CPG;
+          u64 acc[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) acc[k] = 0;
+#pragma unroll
+          for (int sh = 0; sh < 8; ++sh) {
+            uint32_t v[16];
+            tmem_ld16(lane_base + sh * NT + cb, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k] += (u64)(long long)(int32_t)v[k] << (8 * sh);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_tempty[0]);
+          e_read += clock64() - e_a;
+          if (eok) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int n = ntile * NT + cb + k;
+              if (n < A.N) {
+                const long long oi = ((long long)eb * A.N + n) * S + esp;
+                u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                if (A.party == 0 && A.bias) yv += A.bias[n];
+                if (A.res) yv += __ldg(reinterpret_cast<const unsigned long long*>(A.res + oi));  // add_shares
+                A.y[oi] = yv;
+              }
+            }
+          }
+        } else if (cgrp < NGRP) {
 #pragma unroll 1
           for (int c0 = cgrp * CPG; c0 < (cgrp + 1) * CPG; c0 += 8) {
             uint32_t vv[8][8];
@@ -338,6 +376,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&bar_tempty[0]);
+              e_read += clock64() - e_a;
             }
             if (eok) {
 #pragma unroll
@@ -363,8 +402,14 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 #pragma unroll
       for (int p = 0; p < PASSES; ++p, ++u) {
         const int buf = DB ? (u & 1) : 0;
+        e_a = clock64();
         mbar_wait(&bar_tfull[buf], (u / NB) & 1);
         tc_fence_after();
+        {
+          const long long e_b = clock64();
+          e_wait += e_b - e_a;
+          e_a = e_b;
+        }
         const bool last = p == PASSES - 1;
         const uint32_t ubase = lane_base + buf * UCOLS;
         if (cgrp < NGRP) {
@@ -379,6 +424,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&bar_tempty[buf]);
+              e_read += clock64() - e_a;
             }
             u64 acc[8];
             if (last) {
@@ -419,6 +465,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
           if (lane == 0) mbar_arrive(&bar_tempty[buf]);
         }
       }
+    }
+    if ((A.dbg & 4) && A.stamps && warp == 0 && lane == 0) {
+      A.stamps[blockIdx.x * 8 + 6] = e_read;
+      A.stamps[blockIdx.x * 8 + 7] = e_wait;
     }
   }
   tc_fence_before();
@@ -566,6 +616,13 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int grid = A.tiles < sm_count() ? A.tiles : sm_count();
   cudaError_t e;
+  A.stamps = nullptr;
+  if (dbg & 4) {
+    static long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 1024 * 8 * sizeof(long long));
+    A.stamps = buf;
+    hb_tma_last_stamps = buf;
+  }
 #define HB_NTJ(NT_, P_, J_)                                                                                     \
   if (nt == NT_ && J == J_) {                                                                                    \
     e = cudaFuncSetAttribute(k_conv_tma<NT_, P_, J_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \

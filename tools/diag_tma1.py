@@ -22,4 +22,5 @@ if int(os.environ.get("HB_TC_DEBUG", "0")) & 4:
     buf = np.zeros(1024 * 8, dtype=np.int64)
     lib.hb_debug_tma_stamps(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), buf.size)
     st = buf.reshape(-1, 8)[:148]
-    print("MMA warp per CTA (mean clk): total %.0f  wait tmem-empty %.0f  wait full %.0f  issue %.0f  stages %.0f units %.0f" % tuple(st[:, :6].mean(0)))
+    print("MMA warp per CTA (mean clk): total %.0f  wait tmem-empty %.0f  wait full %.0f  issue %.0f  stages %.0f units %.0f"
+          "  | epilogue warp0: tmem read %.0f  wait tfull %.0f" % tuple(st[:, :8].mean(0)))
