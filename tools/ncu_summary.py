@@ -34,6 +34,11 @@ KEEP = [
     "lts__t_bytes.sum",
     "l1tex__t_bytes.sum",
     "smsp__inst_executed.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+    "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.sum",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__m_xbar2l1tex_read_bytes.sum",
 ]
 
 
