@@ -18,6 +18,8 @@ back in the caller's representation.
 
 from __future__ import annotations
 
+import functools
+
 import math
 from dataclasses import dataclass, field
 
@@ -206,10 +208,14 @@ def relu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> Ar
 
 def relu_trace(n: int, window: BitWindow, ring_bits: int, drelu_only: bool = False) -> list:
     """(tag, bytes) of every round, as the reference meter records them."""
+    return list(_relu_trace(n, window.k, window.m, ring_bits, bool(drelu_only)))
+
+
+@functools.lru_cache(maxsize=4096)
+def _relu_trace(n: int, k: int, m: int, ring_bits: int, drelu_only: bool) -> tuple:
     lib = _lib.load()
-    k, m = window.k, window.m
-    return [(_lib.TAG_BY_CODE[lib.hb_relu_round_tag(k, m, r)], int(lib.hb_relu_round_bytes(ring_bits, k, m, n, r)))
-            for r in range(lib.hb_relu_rounds(k, m, int(drelu_only)))]
+    return tuple((_lib.TAG_BY_CODE[lib.hb_relu_round_tag(k, m, r)], int(lib.hb_relu_round_bytes(ring_bits, k, m, n, r)))
+                 for r in range(lib.hb_relu_rounds(k, m, int(drelu_only))))
 
 
 def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitWindow,
@@ -240,10 +246,9 @@ def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitW
     s0.triples.check(need)
     s1.triples.check(need)
     views = [(s.triples.draw(BOOL, w, need[(BOOL, w)]), s.triples.draw(ARITH, N, need[(ARITH, N)])) for s in (s0, s1)]
+    trace = _relu_trace(n, window.k, window.m, N, bool(drelu_only))
     for s in (s0, s1):
-        for tag, nb in relu_trace(n, window, N, drelu_only):
-            with s.endpoint.tag(tag):
-                s.endpoint.meter.record(nb)
+        s.endpoint.meter.record_rounds(trace)
     if host_pipeline:
         return _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only)
     y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
