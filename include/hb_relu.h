@@ -87,6 +87,28 @@ int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, in
  * r-1 from `peer` (NULL for r = 0).  The caller exchanges own/peer between calls
  * (Endpoint.exchange, transport.py:129-133) under tag hb_relu_round_tag(r). */
 size_t hb_relu_workspace_bytes(int k, int m, int64_t n);
+
+/* ---- one party per GPU, openings through the peer's memory (NVLink P2P), one launch per ReLU.
+ * Replaces the per-round Endpoint.exchange loop of protocol.relu / drelu (protocol.py:179-199,
+ * transport.py:129-133) for two parties on two GPUs of one node: the party kernel stores each
+ * round's masked opening of a tile straight into the peer's receive buffer and releases a per-tile
+ * flag; the peer's kernel acquires it.  Same outputs / triple consumption as hb_relu_round.
+ * hb_relu_p2p_bytes: receive-buffer bytes (identical layout on both sides) and the flag count
+ * (uint64 each, zero-initialised once).  seq0 = launches so far x hb_relu_rounds(k, m, drelu_only)
+ * (flags are monotonic).  max_ctas: 0 = 3/4 of the co-resident CTAs, -1 = 1/4 of them (both parties
+ * share one device), > 0 = at most that many.  A peer that does not answer within timeout_s sets *err_dev = 1 (no hang). */
+uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* ntiles);
+int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+                hb_triples_t bool_w, hb_triples_t arith_n, void* recv, const uint64_t* my_flags, void* peer_recv,
+                uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
+                void* stream);
+/* CUDA IPC for the receive buffers / flags of a party on another GPU (64-byte handles); the buffers
+ * are whole allocations (hb_dev_alloc, zero-filled) so a handle maps exactly them. */
+int hb_dev_alloc(uint64_t bytes, void** dev_ptr);
+int hb_dev_free(void* dev_ptr);
+int hb_ipc_export(void* dev_ptr, uint8_t* handle64);
+int hb_ipc_open(const uint8_t* handle64, void** dev_ptr);
+int hb_ipc_close(void* dev_ptr);
 int hb_relu_round(int party, int ring_bits, int k, int m, int64_t n, int round,
                   const uint64_t* x, uint64_t* y, hb_triples_t boolw, hb_triples_t arith,
                   void* workspace, const uint64_t* peer, uint64_t* own, int drelu_only, void* stream);

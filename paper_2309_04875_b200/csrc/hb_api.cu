@@ -11,6 +11,7 @@
 
 #include "../../include/hb_relu.h"
 #include "hb_relu_impl.cuh"
+#include "hb_relu_p2p.cuh"
 #include "hb_ring_tc.cuh"
 #include "hb_conv_tma.cuh"
 
@@ -20,6 +21,9 @@ using hb::u64;
 #define HB_RANGE(lo, hi)                                                                            \
   cudaError_t hb_pair_dispatch_##lo##_##hi(int W, const hb::PairArgs& A, cudaStream_t s);          \
   cudaError_t hb_stage_dispatch_##lo##_##hi(int W, const hb::StageArgs& A, int L, cudaStream_t s); \
+  cudaError_t hb_p2p_dispatch_##lo##_##hi(int W, const hb::P2PArgs& A, int max_ctas, cudaStream_t s); \
+  unsigned long long hb_p2p_layout_##lo##_##hi(int W, unsigned long long n, int drelu_only,        \
+                                               unsigned long long* ntiles);                        \
   size_t hb_pair_smem_##lo##_##hi(int W);
 HB_RANGE(2, 8)
 HB_RANGE(9, 16)
@@ -129,6 +133,16 @@ cudaError_t stage_dispatch(int W, const hb::StageArgs& A, int L, cudaStream_t s)
   return hb_stage_dispatch_57_64(W, A, L, s);
 }
 
+#define HB_RANGE_CALL(fn, W, ...)                              \
+  ((W) <= 8    ? fn##_2_8(W, __VA_ARGS__)                       \
+   : (W) <= 16 ? fn##_9_16(W, __VA_ARGS__)                      \
+   : (W) <= 24 ? fn##_17_24(W, __VA_ARGS__)                     \
+   : (W) <= 32 ? fn##_25_32(W, __VA_ARGS__)                     \
+   : (W) <= 40 ? fn##_33_40(W, __VA_ARGS__)                     \
+   : (W) <= 48 ? fn##_41_48(W, __VA_ARGS__)                     \
+   : (W) <= 56 ? fn##_49_56(W, __VA_ARGS__)                     \
+               : fn##_57_64(W, __VA_ARGS__))
+
 hb::PartyIO make_io(const uint64_t* x, uint64_t* y, const hb_triples_t& bw, const hb_triples_t& ar, int w) {
   hb::PartyIO io;
   io.x = x;
@@ -229,6 +243,72 @@ int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, in
   A.drelu_only = drelu_only ? 1 : 0;
   return cuda_status(pair_dispatch(w, A, S(stream)), "hb_relu_pair");
 }
+
+uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* ntiles) {
+  if (k - m < 2 || k - m > 64 || n < 0) return 0;
+  unsigned long long nt = 0;
+  const uint64_t b = HB_RANGE_CALL(hb_p2p_layout, k - m, (unsigned long long)n, drelu_only, &nt);
+  if (ntiles) *ntiles = (int64_t)nt;
+  return b;
+}
+
+int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+                hb_triples_t boolw, hb_triples_t arith, void* recv, const uint64_t* my_flags, void* peer_recv,
+                uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
+                void* stream) {
+  int rc = check_window(ring_bits, k, m);
+  if (rc) return rc;
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  if (n < 0) return fail(HB_ERR_CONFIG, "negative element count");
+  if (n > 0 && (!recv || !my_flags || !peer_recv || !peer_flags || !err_dev))
+    return fail(HB_ERR_CONFIG, "null p2p buffer");
+  const int w = k - m, L = levels(w);
+  const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
+  if ((rc = check_triples(boolw, "bool", w, nb, party)) || (rc = check_triples(arith, "arith", ring_bits, na, party)))
+    return rc;
+  if (n == 0) return HB_OK;
+  hb::P2PArgs A;
+  A.io = make_io(x, y, boolw, arith, w);
+  A.n = (u64)n;
+  A.N = ring_bits;
+  A.m = m;
+  A.party = party;
+  A.drelu_only = drelu_only ? 1 : 0;
+  A.seq0 = seq0;
+  A.recv = static_cast<uint8_t*>(recv);
+  A.my_flag = reinterpret_cast<const unsigned long long*>(my_flags);
+  A.peer_recv = static_cast<uint8_t*>(peer_recv);
+  A.peer_flag = reinterpret_cast<unsigned long long*>(peer_flags);
+  A.timeout_ns = (u64)(timeout_s * 1e9);
+  A.err = err_dev;
+  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, w, A, max_ctas, S(stream)), "hb_relu_p2p");
+}
+
+int hb_dev_alloc(uint64_t bytes, void** dev_ptr) {
+  // a whole allocation of its own (CUDA IPC maps allocations, not sub-ranges of a caching
+  // allocator's segment), zero-filled
+  cudaError_t e = cudaMalloc(dev_ptr, bytes ? bytes : 1);
+  if (e == cudaSuccess) e = cudaMemset(*dev_ptr, 0, bytes ? bytes : 1);
+  return cuda_status(e, "hb_dev_alloc");
+}
+
+int hb_dev_free(void* dev_ptr) { return cuda_status(cudaFree(dev_ptr), "hb_dev_free"); }
+
+int hb_ipc_export(void* dev_ptr, uint8_t* handle64) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) return cuda_status(e, "hb_ipc_export");
+  memcpy(handle64, &h, sizeof(h));
+  return HB_OK;
+}
+
+int hb_ipc_open(const uint8_t* handle64, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "hb_ipc_open");
+}
+
+int hb_ipc_close(void* dev_ptr) { return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "hb_ipc_close"); }
 
 size_t hb_relu_workspace_bytes(int k, int m, int64_t n) {
   if (k - m < 2 || k - m > 64 || n < 0) return 0;

@@ -3,6 +3,7 @@
 // the 63 window widths compile in parallel (make -j).
 #pragma once
 #include "hb_relu_impl.cuh"
+#include "hb_relu_p2p.cuh"
 
 namespace hb {
 
@@ -84,6 +85,40 @@ cudaError_t HB_CAT(hb_stage_dispatch_, HB_W_LO, HB_W_HI)(int W, const hb::StageA
       break;
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t HB_CAT(hb_p2p_dispatch_, HB_W_LO, HB_W_HI)(int W, const hb::P2PArgs& A, int max_ctas, cudaStream_t s) {
+  switch (W) {
+#define HB_CASE(w) \
+  case w:          \
+    if (w >= HB_W_LO && w <= HB_W_HI) return hb::launch_p2p<(w >= HB_W_LO && w <= HB_W_HI) ? w : HB_W_LO>(A, max_ctas, s); \
+    break;
+#include "hb_widths.inc"
+#undef HB_CASE
+    default:
+      break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+unsigned long long HB_CAT(hb_p2p_layout_, HB_W_LO, HB_W_HI)(int W, unsigned long long n, int drelu_only,
+                                                           unsigned long long* ntiles) {
+  switch (W) {
+#define HB_CASE(w)                                                                                    \
+  case w:                                                                                             \
+    if (w >= HB_W_LO && w <= HB_W_HI) {                                                               \
+      hb::u64 off[hb::P2P_MAXR], nt;                                                                  \
+      const hb::u64 b = hb::p2p_layout<(w >= HB_W_LO && w <= HB_W_HI) ? w : HB_W_LO>(n, drelu_only, off, &nt); \
+      *ntiles = nt;                                                                                   \
+      return b;                                                                                       \
+    }                                                                                                 \
+    break;
+#include "hb_widths.inc"
+#undef HB_CASE
+    default:
+      break;
+  }
+  return 0;
 }
 
 size_t HB_CAT(hb_pair_smem_, HB_W_LO, HB_W_HI)(int W) {

@@ -18,6 +18,7 @@ back in the caller's representation.
 
 from __future__ import annotations
 
+import ctypes
 import functools
 
 import math
@@ -198,12 +199,49 @@ def _relu_staged(session: ProtocolSession, x: ArithShareTensor, window: BitWindo
 
 def drelu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> ArithShareTensor:
     """Shared indicator of x >= 0 on the window [m, k) (protocol.py:179-192)."""
+    if session.endpoint.p2p is not None:
+        return relu_p2p(session, x, window, session.endpoint.p2p, drelu_only=True)
     return _relu_staged(session, x, window, drelu_only=True)
 
 
 def relu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> ArithShareTensor:
     """x * DReLU(x[k:m]), the multiply metered as Mult (protocol.py:195-199)."""
+    if session.endpoint.p2p is not None:
+        return relu_p2p(session, x, window, session.endpoint.p2p, drelu_only=False)
     return _relu_staged(session, x, window, drelu_only=False)
+
+
+def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, link, drelu_only: bool = False,
+             stream=None) -> ArithShareTensor:
+    """One party's ReLU / DReLU in one launch of the NVLink party kernel (hb_relu_p2p): every
+    round's opening goes tile by tile into the peer's receive buffer (`link`, a transport.PeerLink)
+    instead of a per-round Endpoint.exchange.  Same output shares, triple consumption and meter
+    trace as relu() over any endpoint; both parties must call it for the same layers in order."""
+    window.check_fits(x.width)
+    N, k, m, w = x.width, window.k, window.m, window.width
+    xd = _flat(x.data)
+    n = xd.numel()
+    levels = prefix_levels(w)
+    need_a = n if drelu_only else 2 * n
+    session.triples.check({(BOOL, w): n * (1 + 2 * levels), (ARITH, N): need_a})
+    bv = session.triples.draw(BOOL, w, n * (1 + 2 * levels))
+    av = session.triples.draw(ARITH, N, need_a)
+    lib = _lib.load()
+    ntiles = ctypes.c_int64(0)
+    nbytes = lib.hb_relu_p2p_bytes(k, m, n, int(drelu_only), ctypes.byref(ntiles))
+    link.check()
+    link.ensure(nbytes, ntiles.value)
+    rounds = lib.hb_relu_rounds(k, m, int(drelu_only))
+    seq0 = link.seq
+    link.seq += rounds
+    session.endpoint.meter.record_rounds(_relu_trace(n, k, m, N, bool(drelu_only)))
+    y = torch.empty(n, dtype=torch.int64, device=xd.device)
+    st = _stream() if stream is None else stream.cuda_stream
+    _lib.check(lib.hb_relu_p2p(session.party, N, k, m, n, xd.data_ptr(), y.data_ptr(), bv.abi(), av.abi(),
+                               link.recv, link.flags, link.peer_recv, link.peer_flags, seq0,
+                               link.max_ctas, link.timeout_s, link.err.data_ptr(), int(drelu_only), st))
+    link.after_launch(torch.cuda.current_stream() if stream is None else stream)
+    return _wrap(ArithShareTensor, x.party, N, y, x.data, x.shape)
 
 
 def relu_trace(n: int, window: BitWindow, ring_bits: int, drelu_only: bool = False) -> list:

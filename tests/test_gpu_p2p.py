@@ -1,0 +1,170 @@
+"""GPU parity of the one-launch NVLink party kernel (hb_relu_p2p, protocol.relu_p2p).
+
+The kernel is written for one party per GPU with the peer's receive buffer mapped over NVLink.
+This run has one GPU, so the parties run as two streams of one process on the same device, each
+PeerLink pointing at the other's buffers (transport.local_p2p_pair) -- the same kernel, flags and
+fences; only the "remote" stores land in local HBM.  A second test runs the two parties as two
+processes on the one GPU with the buffers exchanged as CUDA IPC handles (the multi-GPU plumbing).
+Bar: bit-exact per-party shares against the oracle and the fused pair kernel.
+"""
+
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import golden_cases as gc
+from hb_helpers import stocked_sessions_for_relu
+from oracle import hb_oracle as O
+from paper_2309_04875_b200 import protocol, sharing, transport
+from paper_2309_04875_b200.errors import TransportError
+from paper_2309_04875_b200.ring import BitWindow
+from paper_2309_04875_b200.sharing import ArithShareTensor
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_share(t):
+    if isinstance(t.data, torch.Tensor):
+        return t, False
+    return ArithShareTensor(t.party, t.width, torch.from_numpy(np.ascontiguousarray(t.data).view(np.int64)).cuda()), True
+
+
+def _p2p_pair(s0, s1, t0, t1, win, links, drelu_only=False):
+    # inputs on the device first: a pageable host copy between the two launches would wait for
+    # party 0's kernel, which is waiting for party 1 (one device, one process)
+    (t0, host), (t1, _) = _dev_share(t0), _dev_share(t1)
+    cur = torch.cuda.current_stream()
+    st = (torch.cuda.Stream(), torch.cuda.Stream())
+    out = []
+    for s, t, lk, strm in zip((s0, s1), (t0, t1), links, st):
+        strm.wait_stream(cur)
+        with torch.cuda.stream(strm):
+            out.append(protocol.relu_p2p(s, t, win, lk, drelu_only=drelu_only, stream=strm))
+    for strm in st:
+        cur.wait_stream(strm)
+    torch.cuda.synchronize()
+    for lk in links:
+        lk.check(sync=True)
+    if host:
+        out = [ArithShareTensor(o.party, o.width, o.data.cpu().numpy().view(np.uint64)) for o in out]
+    return out
+
+
+@pytest.mark.parametrize("k,m", [(64, 0), (32, 0), (22, 6), (22, 14), (22, 16), (13, 0), (40, 3)])
+def test_p2p_vs_oracle_per_party(k, m):
+    n = (1 << 16) + 37  # a partial last tile
+    x0, x1 = gc.baseline_inputs(n, seed=5)
+    w = k - m
+    curs = O.stocked_cursors(n, w, 64, seed=6)
+    y0o, y1o, _, _ = O.relu_pair(x0, x1, 64, k, m, curs)
+    s0, s1, eps = stocked_sessions_for_relu(n, w, 64, seed=6)
+    t0, t1 = ArithShareTensor(0, 64, torch.from_numpy(x0.view(np.int64)).cuda()), \
+        ArithShareTensor(1, 64, torch.from_numpy(x1.view(np.int64)).cuda())
+    r0, r1 = _p2p_pair(s0, s1, t0, t1, BitWindow(k, m), transport.local_p2p_pair())
+    assert np.array_equal(r0.data.cpu().numpy().view(np.uint64), y0o)
+    assert np.array_equal(r1.data.cpu().numpy().view(np.uint64), y1o)
+    # the reference meter trace, per party
+    for ep in eps:
+        assert ep.meter.trace == protocol.relu_trace(n, BitWindow(k, m), 64)
+
+
+@pytest.mark.parametrize("w", [2, 3, 5, 6, 7, 8, 9, 12, 16, 17, 24, 31, 33, 48, 63, 64])
+def test_p2p_widths_and_drelu(w):
+    n = 3000
+    k, m = (w, 0) if w % 2 else (min(64, w + 5), min(64, w + 5) - w)
+    x0, x1 = gc.baseline_inputs(n, seed=w + 100)
+    curs = O.stocked_cursors(n, w, 64, seed=w)
+    y0o, y1o, _, _ = O.relu_pair(x0, x1, 64, k, m, curs)
+    s0, s1, _ = stocked_sessions_for_relu(n, w, 64, seed=w)
+    t0, t1 = ArithShareTensor(0, 64, x0), ArithShareTensor(1, 64, x1)
+    r0, r1 = _p2p_pair(s0, s1, t0, t1, BitWindow(k, m), transport.local_p2p_pair())
+    assert np.array_equal(r0.data, y0o) and np.array_equal(r1.data, y1o)
+    # DReLU through the same kernel reconstructs to the windowed sign
+    s0, s1, _ = stocked_sessions_for_relu(n, w, 64, seed=w + 1)
+    d0, d1 = _p2p_pair(s0, s1, t0, t1, BitWindow(k, m), transport.local_p2p_pair(), drelu_only=True)
+    assert np.array_equal(sharing.reconstruct_arith(d0, d1), O.drelu_from_shares(x0, x1, 64, k, m))
+
+
+def test_p2p_sequence_growth_and_large():
+    """Several layers in a row on the same links (monotonic flags, buffer growth), then 2^22."""
+    links = transport.local_p2p_pair()
+    for i, logn in enumerate((12, 18, 14, 22)):
+        n = (1 << logn) + i
+        k, m = (22, 14) if i % 2 == 0 else (64, 0)
+        x0, x1 = gc.baseline_inputs(n, seed=logn)
+        s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=logn)
+        t0 = ArithShareTensor(0, 64, torch.from_numpy(x0.view(np.int64)).cuda())
+        t1 = ArithShareTensor(1, 64, torch.from_numpy(x1.view(np.int64)).cuda())
+        r0, r1 = _p2p_pair(s0, s1, t0, t1, BitWindow(k, m), links)
+        s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=logn)
+        q0, q1 = protocol.relu_pair((s0, s1), t0, t1, BitWindow(k, m))
+        assert torch.equal(r0.data, q0.data) and torch.equal(r1.data, q1.data)
+
+
+def test_p2p_missing_peer_times_out():
+    """Only party 0 runs: its kernel gives up after the timeout and the link raises."""
+    links = transport.local_p2p_pair()
+    links[0].timeout_s = 0.05
+    n = 4096
+    x0, _ = gc.baseline_inputs(n, seed=1)
+    s0, _, _ = stocked_sessions_for_relu(n, 8, 64, seed=1)
+    protocol.relu_p2p(s0, ArithShareTensor(0, 64, x0), BitWindow(22, 14), links[0])
+    with pytest.raises(TransportError):
+        links[0].check(sync=True)
+
+
+_CHILD = r"""
+import os, sys
+sys.path.insert(0, os.environ["HB_ROOT"]); sys.path.insert(0, os.path.join(os.environ["HB_ROOT"], "tests"))
+import numpy as np, torch, torch.distributed as dist
+import golden_cases as gc
+from hb_helpers import stocked_sessions_for_relu
+from paper_2309_04875_b200 import protocol, transport
+from paper_2309_04875_b200.protocol import ProtocolSession
+from paper_2309_04875_b200.ring import BitWindow
+from paper_2309_04875_b200.sharing import ArithShareTensor
+rank = int(os.environ["RANK"])
+dist.init_process_group("gloo", rank=rank, world_size=2)
+n, k, m = 20000, 22, 14
+x0, x1 = gc.baseline_inputs(n, seed=3)
+s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=3)
+sess = (s0, s1)[rank]
+ep = transport.DistEndpoint(rank, 1 - rank)
+ep.enable_p2p(timeout_s=60.0)
+session = ProtocolSession(ep, sess.triples)
+x = ArithShareTensor(rank, 64, torch.from_numpy((x0, x1)[rank].view(np.int64)).cuda())
+y = protocol.relu(session, x, BitWindow(k, m))
+ep.p2p.check(sync=True)
+np.save(os.environ["HB_OUT"] + f"/y{rank}.npy", y.data.cpu().numpy())
+dist.barrier()
+ep.p2p.close()
+dist.destroy_process_group()
+"""
+
+
+def test_p2p_two_processes_ipc(tmp_path):
+    """Two party processes on the one GPU, receive buffers exchanged as CUDA IPC handles over a
+    gloo group (the multi-GPU plumbing; kernels of two processes time-slice on one device)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   HB_ROOT=root, HB_OUT=str(tmp_path))
+        procs.append(subprocess.Popen([sys.executable, "-c", _CHILD], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT))
+    outs = [p.communicate(timeout=300)[0].decode(errors="replace") for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    y0, y1 = np.load(tmp_path / "y0.npy"), np.load(tmp_path / "y1.npy")
+    x0, x1 = gc.baseline_inputs(20000, seed=3)
+    s0, s1, _ = stocked_sessions_for_relu(20000, 8, 64, seed=3)
+    q0, q1 = protocol.relu_pair((s0, s1), ArithShareTensor(0, 64, x0), ArithShareTensor(1, 64, x1), BitWindow(22, 14))
+    assert np.array_equal(y0.view(np.uint64), np.asarray(q0.data).view(np.uint64))
+    assert np.array_equal(y1.view(np.uint64), np.asarray(q1.data).view(np.uint64))
