@@ -49,7 +49,10 @@ def parse():
     p.add_argument("--k", type=int, default=22)
     p.add_argument("--m", type=int, default=14)
     p.add_argument("--ring-bits", type=int, default=64)
-    p.add_argument("--path", choices=["pair", "staged"], default="pair", help="N=1 driver")
+    p.add_argument("--path", choices=["pair", "staged", "p2p"], default="pair",
+                   help="N=1 driver: fused pair kernel, staged rounds, or the P2P party kernels on two streams")
+    p.add_argument("--multi-path", choices=["p2p", "nccl"], default="p2p",
+                   help="N>1: one-launch NVLink party kernel (peer buffers over CUDA IPC) or staged rounds + NCCL")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-resnet", action="store_true", help="skip the ResNet18 secondary measurement")
@@ -213,6 +216,8 @@ def run_single(args):
     sets = stock_sets(stores, (0, 1), n, w, N, L, args.triple_gb, args.steps + args.warmup, seed=99)
     need = {(dealer.BOOL, w): n * (1 + 2 * L), (dealer.ARITH, N): 2 * n}
     s = torch.cuda.current_stream()
+    if args.path == "p2p":
+        links = transport.local_p2p_pair()
 
     def step(a0, a1):
         if stores[0].remaining(dealer.BOOL, w) < need[(dealer.BOOL, w)]:
@@ -221,6 +226,8 @@ def run_single(args):
                 st.rewind(dealer.ARITH, N)
         if args.path == "pair":
             return protocol.relu_pair(sessions, ArithShareTensor(0, N, a0), ArithShareTensor(1, N, a1), win)
+        if args.path == "p2p":  # both party kernels in one launch on this device, openings via peer buffers
+            return protocol.relu_p2p_pair(sessions, ArithShareTensor(0, N, a0), ArithShareTensor(1, N, a1), win, links)
         return transport.run_parties(lambda: protocol.relu(sessions[0], ArithShareTensor(0, N, a0), win),
                                      lambda: protocol.relu(sessions[1], ArithShareTensor(1, N, a1), win))
 
@@ -246,7 +253,9 @@ def run_single(args):
 
     bpe = algorithmic_bytes_per_elem(w, N, L)
     peak, peak_src = peaks()
-    alg_bytes = 2 * n * bpe["fused"]
+    # the P2P kernels write the openings to the peer's buffer and read the peer's: SURVEY H(w)
+    alg_bpe = bpe["survey_H"] if args.path == "p2p" else bpe["fused"]
+    alg_bytes = 2 * n * alg_bpe
     achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
     try:
@@ -258,9 +267,12 @@ def run_single(args):
     except (OSError, ValueError, KeyError):
         pass
 
+    if args.path == "p2p":
+        for lk in links:
+            lk.check(sync=True)
     # ---- e2e: the public API with host (pinned) buffers, H2D + D2H inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.path == "pair":
         h0 = x0.cpu().pin_memory()
         h1 = x1.cpu().pin_memory()
         torch.cuda.synchronize()
@@ -298,16 +310,19 @@ def run_single(args):
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"secure ReLU layer n=2^{args.logn}, window ({k},{m}) w={w}, N={N}",
                    "n": n, "window": [k, m], "ring_bits": N, "parties": "1 pair time-sliced on 1 GPU",
-                   "path": "fused pair kernel hb_relu_pair" if args.path == "pair" else "staged hb_relu_round x2",
+                   "path": {"pair": "fused pair kernel hb_relu_pair", "staged": "staged hb_relu_round x2",
+                            "p2p": "both parties' NVLink party kernels in one launch (hb_relu_p2p_pair), openings via "
+                                   "each other's receive buffers"}[args.path],
                    "inputs": "x_f~N(0,4^2), f=16, additive shares; Beaver triples from the on-device dealer",
                    "triple_sets": sets, "l2": f"inputs {2 * n * bpe['fused'] / 1e9:.2f} GB/step > 126 MB L2",
                    "parallelism": "pair"},
         "correct": ok,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_elem_per_party": bpe["fused"], "survey_H_bytes_per_elem_per_party": bpe["survey_H"],
+                     "alg_bytes_per_elem_per_party": alg_bpe, "survey_H_bytes_per_elem_per_party": bpe["survey_H"],
                      "frac_vs_survey_H": (2 * n * bpe["survey_H"] / (launch_ms / 1e3) / 1e9) / peak,
-                     "kernel": f"hb::k_relu_pair<{w},128>", "launch_ms": launch_ms},
+                     "kernel": f"hb::k_relu_pair<{w},128>" if args.path != "p2p" else f"hb::k_relu_p2p<{w}> x2",
+                     "launch_ms": launch_ms},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
         "resnet18": resnet,
     }
@@ -426,6 +441,9 @@ def run_multi(args):
     L = protocol.prefix_levels(w)
     win = BitWindow(k, m)
     ep = transport.DistEndpoint(party, rank ^ 1) if active else None
+    if active and args.multi_path == "p2p" and ep.enable_p2p() is None:
+        log(f"[rank {rank}] NVLink P2P mapping unavailable: staged rounds + {args.backend}")
+    used_p2p = bool(active and ep.p2p is not None)
     store = dealer.TripleStore(party)
     s = torch.cuda.current_stream()
     if active:
@@ -484,9 +502,12 @@ def run_multi(args):
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"secure ReLU layer n=2^{args.logn} per pair, window ({k},{m}) w={w}, N={N}",
                        "n_per_pair": n, "pairs": pairs, "window": [k, m], "ring_bits": N,
-                       "path": f"staged hb_relu_round + {args.backend} send/recv per round (ranks 2i<->2i+1)",
+                       "path": ("one-launch NVLink party kernel hb_relu_p2p, openings stored into the peer's "
+                                "buffer (CUDA IPC) with per-chunk flags (ranks 2i<->2i+1)") if used_p2p
+                       else f"staged hb_relu_round + {args.backend} send/recv per round (ranks 2i<->2i+1)",
                        "parallelism": f"{pairs} party pairs"},
-            "gpu_launches": args.steps * (L + 4), "clocks": clk.summary(), "correct": bool(ok.item() > 0.5),
+            "gpu_launches": args.steps * (1 if used_p2p else L + 4), "clocks": clk.summary(),
+            "correct": bool(ok.item() > 0.5),
             "e2e": None,
         }
     dist.destroy_process_group()
@@ -513,6 +534,9 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
     s = torch.cuda.current_stream()
     if active:
         ep = transport.DistEndpoint(party, rank ^ 1)
+        if args.multi_path == "p2p" and ep.enable_p2p() is None:
+            log(f"[rank {rank}] NVLink P2P mapping unavailable: staged rounds + {args.backend}")
+        used_p2p = ep.p2p is not None
         store = dealer.TripleStore(party)
         need = nn.triple_requirements(model, cfg, per_pair)
         for i, ((kind, width), count) in enumerate(sorted(need.items())):
@@ -559,7 +583,9 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"{args.workload} private inference, batch {pairs * per_pair} over {pairs} pairs",
                        "batch": pairs * per_pair, "batch_per_pair": per_pair, "pairs": pairs,
-                       "path": f"nn.model_forward per party, staged ReLU + {args.backend} send/recv per round",
+                       "path": "nn.model_forward per party, ReLU " + (
+                           "one-launch NVLink party kernel (openings into the peer's buffer)" if used_p2p
+                           else f"staged + {args.backend} send/recv per round"),
                        "parallelism": f"{pairs} party pairs"},
             "clocks": clk.summary(), "e2e": None,
         }

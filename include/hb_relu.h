@@ -95,13 +95,20 @@ size_t hb_relu_workspace_bytes(int k, int m, int64_t n);
  * flag; the peer's kernel acquires it.  Same outputs / triple consumption as hb_relu_round.
  * hb_relu_p2p_bytes: receive-buffer bytes (identical layout on both sides) and the flag count
  * (uint64 each, zero-initialised once).  seq0 = launches so far x hb_relu_rounds(k, m, drelu_only)
- * (flags are monotonic).  max_ctas: 0 = 3/4 of the co-resident CTAs, -1 = 1/4 of them (both parties
- * share one device), > 0 = at most that many.  A peer that does not answer within timeout_s sets *err_dev = 1 (no hang). */
+ * (flags are monotonic).  max_ctas: 0 = 3/4 of the co-resident CTAs, > 0 = at most
+ * that many.  A peer that does not answer within timeout_s sets *err_dev = 1 (no hang). */
 uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* ntiles);
 int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
                 hb_triples_t bool_w, hb_triples_t arith_n, void* recv, const uint64_t* my_flags, void* peer_recv,
                 uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
                 void* stream);
+/* Both parties' party kernels in ONE launch on one device (CTAs split between the parties), the
+ * openings going through each other's receive buffers exactly as across two GPUs: the single-GPU
+ * harness of hb_relu_p2p (recv1 / flags1 play the peer's mapped buffers for party 0 and vice versa). */
+int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
+                     uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas,
+                     double timeout_s, int* err_dev, int drelu_only, void* stream);
 /* CUDA IPC for the receive buffers / flags of a party on another GPU (64-byte handles); the buffers
  * are whole allocations (hb_dev_alloc, zero-filled) so a handle maps exactly them. */
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr);

@@ -21,7 +21,8 @@ using hb::u64;
 #define HB_RANGE(lo, hi)                                                                            \
   cudaError_t hb_pair_dispatch_##lo##_##hi(int W, const hb::PairArgs& A, cudaStream_t s);          \
   cudaError_t hb_stage_dispatch_##lo##_##hi(int W, const hb::StageArgs& A, int L, cudaStream_t s); \
-  cudaError_t hb_p2p_dispatch_##lo##_##hi(int W, const hb::P2PArgs& A, int max_ctas, cudaStream_t s); \
+  cudaError_t hb_p2p_dispatch_##lo##_##hi(int W, const hb::P2PArgs& A, const hb::P2PArgs* B, int max_ctas, \
+                                          cudaStream_t s);                                             \
   unsigned long long hb_p2p_layout_##lo##_##hi(int W, unsigned long long n, int drelu_only,        \
                                                unsigned long long* ntiles);                        \
   size_t hb_pair_smem_##lo##_##hi(int W);
@@ -252,10 +253,11 @@ uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* nti
   return b;
 }
 
-int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
-                hb_triples_t boolw, hb_triples_t arith, void* recv, const uint64_t* my_flags, void* peer_recv,
-                uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
-                void* stream) {
+namespace {
+int p2p_args(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+             const hb_triples_t& boolw, const hb_triples_t& arith, void* recv, const uint64_t* my_flags,
+             void* peer_recv, uint64_t* peer_flags, uint64_t seq0, double timeout_s, int* err_dev, int drelu_only,
+             hb::P2PArgs& A) {
   int rc = check_window(ring_bits, k, m);
   if (rc) return rc;
   if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
@@ -266,8 +268,6 @@ int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_
   const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
   if ((rc = check_triples(boolw, "bool", w, nb, party)) || (rc = check_triples(arith, "arith", ring_bits, na, party)))
     return rc;
-  if (n == 0) return HB_OK;
-  hb::P2PArgs A;
   A.io = make_io(x, y, boolw, arith, w);
   A.n = (u64)n;
   A.N = ring_bits;
@@ -281,7 +281,34 @@ int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_
   A.peer_flag = reinterpret_cast<unsigned long long*>(peer_flags);
   A.timeout_ns = (u64)(timeout_s * 1e9);
   A.err = err_dev;
-  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, w, A, max_ctas, S(stream)), "hb_relu_p2p");
+  return HB_OK;
+}
+}  // namespace
+
+int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+                hb_triples_t boolw, hb_triples_t arith, void* recv, const uint64_t* my_flags, void* peer_recv,
+                uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
+                void* stream) {
+  hb::P2PArgs A;
+  const int rc = p2p_args(party, ring_bits, k, m, n, x, y, boolw, arith, recv, my_flags, peer_recv, peer_flags, seq0,
+                          timeout_s, err_dev, drelu_only, A);
+  if (rc || n == 0) return rc;
+  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A, (const hb::P2PArgs*)nullptr, max_ctas, S(stream)),
+                     "hb_relu_p2p");
+}
+
+int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
+                     uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas,
+                     double timeout_s, int* err_dev, int drelu_only, void* stream) {
+  hb::P2PArgs A0, A1;
+  int rc = p2p_args(0, ring_bits, k, m, n, x0, y0, bool0, arith0, recv0, flags0, recv1, flags1, seq0, timeout_s,
+                    err_dev, drelu_only, A0);
+  if (rc) return rc;
+  rc = p2p_args(1, ring_bits, k, m, n, x1, y1, bool1, arith1, recv1, flags1, recv0, flags0, seq0, timeout_s, err_dev,
+                drelu_only, A1);
+  if (rc || n == 0) return rc;
+  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A0, &A1, max_ctas, S(stream)), "hb_relu_p2p_pair");
 }
 
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr) {

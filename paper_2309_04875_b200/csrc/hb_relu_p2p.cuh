@@ -18,8 +18,9 @@
 // the arithmetic rounds send uint64 per element.  The reference meter records the reference
 // payload sizes (relu_trace); the wire carries the same bytes for w in {8, 16, 32, 64}.
 //
-// Deadlock freedom: the grid is persistent and co-resident with margin (3/4 of the occupancy, 1/4
-// when both parties share one device), so CTA c of either party always reaches tile t.  A bounded spin (globaltimer, ~timeout_ms) turns a missing peer into an
+// Deadlock freedom: the grid is persistent and co-resident with margin (3/4 of the occupancy; both
+// parties in one grid at 3/8 each when they share a device, k_relu_p2p_dual), so CTA c of either
+// party always reaches tile t.  A bounded spin (globaltimer, ~timeout_ms) turns a missing peer into an
 // error flag instead of a hang.
 #pragma once
 #include <cstdio>
@@ -29,7 +30,8 @@
 
 namespace hb {
 
-constexpr int P2P_TP = 128;      // threads (groups) per CTA = one tile
+constexpr int P2P_TP = 128;      // threads per CTA
+constexpr int P2P_C = 4;         // groups per thread per chunk (the unit of synchronisation)
 constexpr int P2P_MAXR = 10;     // rounds per ReLU <= L + 3 with L <= 6
 
 struct P2PArgs {
@@ -73,12 +75,17 @@ HB_DEV unsigned long long globaltimer() {
   return t;
 }
 
+// Round-major chunks: a CTA's unit of synchronisation is a chunk of P2P_C x P2P_TP groups (thread t
+// owns groups t, t + TP, ..: coalesced), so one flag round trip is amortised over 4x more elements
+// than a one-group-per-thread tile.  Between rounds each thread keeps only the protocol state of its
+// groups in registers (S, G, P, sign, d); each round's triple segment is loaded in that round (every
+// segment is used by exactly one round) and x is re-read for the final multiply.
 template <int W, bool RING64>
-__global__ void __launch_bounds__(P2P_TP) k_relu_p2p(const P2PArgs A) {
+__device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, const unsigned ncta) {
   using G = Geo<W>;
   using K = Kit<W>;
   using PG = P2PGeo<W>;
-  constexpr int GS = G::GS, PW = G::PW, L = K::L, NSEG = 1 + 2 * L, UB = PG::UB, NU = PG::NU;
+  constexpr int GS = G::GS, PW = G::PW, L = K::L, UB = PG::UB, NU = PG::NU, C = P2P_C;
   constexpr int TP = P2P_TP;
   __shared__ int abort_s;
   const int t = threadIdx.x;
@@ -89,43 +96,46 @@ __global__ void __launch_bounds__(P2P_TP) k_relu_p2p(const P2PArgs A) {
   const bool mult = !A.drelu_only;
   if (t == 0) abort_s = 0;
 
-  for (u64 tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const u64 e0 = (tile * TP + t) * GS;
-    const int valid = e0 >= n ? 0 : (int)min((u64)GS, n - e0);
-
-    // round r: my words k of this tile -> peer, then wait for the peer's and read them locally
-    auto wire = [&](uint8_t* base, int r, int k) -> uint8_t* {  // unit k of this thread in round r
+  for (u64 tile = cta; tile < A.ntiles; tile += ncta) {
+    u64 e0[C];
+    int valid[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      e0[c] = ((tile * C + c) * TP + t) * GS;
+      valid[c] = e0[c] >= n ? 0 : (int)min((u64)GS, n - e0[c]);
+    }
+    // unit k of group c of this thread in round r: [round][tile][k][c][t]
+    auto wire = [&](uint8_t* base, int r, int k, int c) -> uint8_t* {
       const int ru = PG::round_unit(r);
-      return base + A.round_off[r] + ((tile * (PG::round_bytes(r) / ru) + k) * TP + t) * ru;
+      return base + A.round_off[r] + (((tile * (PG::round_bytes(r) / ru) + k) * C + c) * TP + t) * ru;
     };
-    auto put_group = [&](int r, int k0, const Cg<W>& v) {
+    auto put_group = [&](int r, int k0, int c, const Cg<W>& v) {
       const Pk<W> p = to_packed<W>(v);
       if constexpr (UB == 4) {
-        *reinterpret_cast<uint32_t*>(wire(A.peer_recv, r, k0)) = (uint32_t)p.v[0];
+        *reinterpret_cast<uint32_t*>(wire(A.peer_recv, r, k0, c)) = (uint32_t)p.v[0];
       } else {
 #pragma unroll
-        for (int q = 0; q < PW; ++q) *reinterpret_cast<u64*>(wire(A.peer_recv, r, k0 + q)) = p.v[q];
+        for (int q = 0; q < PW; ++q) *reinterpret_cast<u64*>(wire(A.peer_recv, r, k0 + q, c)) = p.v[q];
       }
     };
-    auto get_group = [&](int r, int k0) -> Cg<W> {
+    auto get_group = [&](int r, int k0, int c) -> Cg<W> {
       Pk<W> p;
       if constexpr (UB == 4) {
-        p.v[0] = (u64)__ldcg(reinterpret_cast<const unsigned int*>(wire(A.recv, r, k0)));
+        p.v[0] = (u64)__ldcg(reinterpret_cast<const unsigned int*>(wire(A.recv, r, k0, c)));
 #pragma unroll
         for (int q = 1; q < PW; ++q) p.v[q] = 0;
       } else {
 #pragma unroll
         for (int q = 0; q < PW; ++q)
-          p.v[q] = (u64)__ldcg(reinterpret_cast<const unsigned long long*>(wire(A.recv, r, k0 + q)));
+          p.v[q] = (u64)__ldcg(reinterpret_cast<const unsigned long long*>(wire(A.recv, r, k0 + q, c)));
       }
       return from_packed<W>(p);
     };
-    auto put_word = [&](int r, int k, u64 v) { *reinterpret_cast<u64*>(wire(A.peer_recv, r, k)) = v; };
-    auto get_word = [&](int r, int k) -> u64 {
-      return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(wire(A.recv, r, k)));
+    auto put_word = [&](int r, int k, int c, u64 v) { *reinterpret_cast<u64*>(wire(A.peer_recv, r, k, c)) = v; };
+    auto get_word = [&](int r, int k, int c) -> u64 {
+      return (u64)__ldcg(reinterpret_cast<const unsigned long long*>(wire(A.recv, r, k, c)));
     };
-    // release round r of this tile to the peer, then acquire the peer's round r
-    auto exchange = [&](int r) -> bool {
+    auto exchange = [&](int r) -> bool {  // release round r of this chunk, acquire the peer's
       __syncthreads();
       if (t == 0) {
         const unsigned long long seq = A.seq0 + (u64)r + 1;
@@ -143,117 +153,156 @@ __global__ void __launch_bounds__(P2P_TP) k_relu_p2p(const P2PArgs A) {
       __syncthreads();
       return abort_s == 0;
     };
+    auto bseg = [&](const u64* arr, int sgi, int c) { return load_cg<W>(arr, io.bcur + (u64)sgi * n + e0[c], io.bnw); };
 
-    // ---- loads up front, as in k_relu_pair
-    u64 x[GS];
-    load_u64s<GS>(io.x + e0, valid, x);
-    Cg<W> ta[NSEG], tbv[NSEG], tc[NSEG];
-#pragma unroll
-    for (int sgi = 0; sgi < NSEG; ++sgi) {
-      const u64 e = io.bcur + (u64)sgi * n + e0;
-      ta[sgi] = load_cg<W>(io.ba, e, io.bnw);
-      tbv[sgi] = load_cg<W>(io.bb, e, io.bnw);
-      tc[sgi] = load_cg<W>(io.bc, e, io.bnw);
-    }
-    u64 a1[GS], b1[GS], c1[GS], a2[GS], b2[GS], c2[GS];
-    const u64 ta0 = io.acur + e0;
-    load_u64s<GS>(io.aa + ta0, valid, a1);
-    load_u64s<GS>(io.ab + ta0, valid, b1);
-    load_u64s<GS>(io.ac + ta0, valid, c1);
-    if (mult) {
-      load_u64s<GS>(io.aa + ta0 + n, valid, a2);
-      load_u64s<GS>(io.ab + ta0 + n, valid, b2);
-      load_u64s<GS>(io.ac + ta0 + n, valid, c2);
-    }
-
-    const Cg<W> S = K::slice(x, A.m);
-
-    // ---- round 0: generate bits
-    Cg<W> Gc, P = S;
+    Cg<W> S[C], Gc[C], P[C];
+    // ---- round 0: slice, generate-bit AND
     {
-      const Cg<W> z0 = cg_zero<W>();
-      const Cg<W> e = (p0 ? S : z0) ^ ta[0];
-      const Cg<W> f = (p0 ? z0 : S) ^ tbv[0];
-      put_group(0, 0, e);
-      put_group(0, NU, f);
+      Cg<W> e[C], f[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        u64 x[GS];
+        load_u64s<GS>(io.x + e0[c], valid[c], x);
+        S[c] = K::slice(x, A.m);
+        P[c] = S[c];
+        const Cg<W> z0 = cg_zero<W>();
+        e[c] = (p0 ? S[c] : z0) ^ bseg(io.ba, 0, c);
+        f[c] = (p0 ? z0 : S[c]) ^ bseg(io.bb, 0, c);
+        put_group(0, 0, c, e[c]);
+        put_group(0, NU, c, f[c]);
+      }
       if (!exchange(0)) return;
-      Gc = K::and_z(p0, e ^ get_group(0, 0), f ^ get_group(0, NU), ta[0], tbv[0], tc[0]);
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        Gc[c] = K::and_z(p0, e[c] ^ get_group(0, 0, c), f[c] ^ get_group(0, NU, c), bseg(io.ba, 0, c),
+                         bseg(io.bb, 0, c), bseg(io.bc, 0, c));
     }
     // ---- rounds 1..L: Kogge-Stone levels
-#pragma unroll
+#pragma unroll 1
     for (int l = 0; l < L; ++l) {
       const int r = 1 + l, sg = 1 + 2 * l, sp = 2 + 2 * l;
-      Cg<W> o[4];
-      K::level_open(p0, l, Gc, P, ta[sg], tbv[sg], ta[sp], tbv[sp], o);
+      Cg<W> o[C][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) put_group(r, q * NU, o[q]);
-      if (!exchange(r)) return;
-      const Cg<W> zg = K::and_z(p0, o[0] ^ get_group(r, 0), o[2] ^ get_group(r, 2 * NU), ta[sg], tbv[sg], tc[sg]);
-      const Cg<W> zp = K::and_z(p0, o[1] ^ get_group(r, NU), o[3] ^ get_group(r, 3 * NU), ta[sp], tbv[sp], tc[sp]);
-      Gc = Gc ^ zg;
-      P = zp;
-    }
-    // ---- round L+1: B2A of the sign bit
-    const unsigned sgn = K::sign_bits(S, Gc);
-    u64 d[GS];
-    {
-      const int r = L + 1;
-      u64 e1[GS], f1[GS];
+      for (int c = 0; c < C; ++c) {
+        K::level_open(p0, l, Gc[c], P[c], bseg(io.ba, sg, c), bseg(io.bb, sg, c), bseg(io.ba, sp, c),
+                      bseg(io.bb, sp, c), o[c]);
 #pragma unroll
-      for (int j = 0; j < GS; ++j) {
-        const u64 bit = (sgn >> j) & 1u;
-        e1[j] = ((p0 ? bit : 0ull) - a1[j]) & MN;
-        f1[j] = ((p0 ? 0ull : bit) - b1[j]) & MN;
-        put_word(r, j, e1[j]);
-        put_word(r, GS + j, f1[j]);
+        for (int q = 0; q < 4; ++q) put_group(r, q * NU, c, o[c][q]);
       }
       if (!exchange(r)) return;
 #pragma unroll
-      for (int j = 0; j < GS; ++j) {
-        const u64 E = (e1[j] + get_word(r, j)) & MN;
-        const u64 F = (f1[j] + get_word(r, GS + j)) & MN;
-        const u64 tt = mul_z(p0, E, F, a1[j], b1[j], c1[j], MN);
-        const u64 bit = (sgn >> j) & 1u;
-        d[j] = ((p0 ? 1ull : 0ull) - ((bit - 2 * tt) & MN)) & MN;
+      for (int c = 0; c < C; ++c) {
+        const Cg<W> zg = K::and_z(p0, o[c][0] ^ get_group(r, 0, c), o[c][2] ^ get_group(r, 2 * NU, c),
+                                  bseg(io.ba, sg, c), bseg(io.bb, sg, c), bseg(io.bc, sg, c));
+        const Cg<W> zp = K::and_z(p0, o[c][1] ^ get_group(r, NU, c), o[c][3] ^ get_group(r, 3 * NU, c),
+                                  bseg(io.ba, sp, c), bseg(io.bb, sp, c), bseg(io.bc, sp, c));
+        Gc[c] = Gc[c] ^ zg;
+        P[c] = zp;
+      }
+    }
+    // ---- round L+1: B2A of the sign bit
+    u64 d[C][GS];
+    {
+      const int r = L + 1;
+      unsigned sgn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        sgn[c] = K::sign_bits(S[c], Gc[c]);
+        u64 a1[GS], b1[GS];
+        load_u64s<GS>(io.aa + io.acur + e0[c], valid[c], a1);
+        load_u64s<GS>(io.ab + io.acur + e0[c], valid[c], b1);
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          const u64 bit = (sgn[c] >> j) & 1u;
+          put_word(r, j, c, ((p0 ? bit : 0ull) - a1[j]) & MN);
+          put_word(r, GS + j, c, ((p0 ? 0ull : bit) - b1[j]) & MN);
+        }
+      }
+      if (!exchange(r)) return;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        u64 a1[GS], b1[GS], c1[GS];
+        load_u64s<GS>(io.aa + io.acur + e0[c], valid[c], a1);
+        load_u64s<GS>(io.ab + io.acur + e0[c], valid[c], b1);
+        load_u64s<GS>(io.ac + io.acur + e0[c], valid[c], c1);
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          const u64 bit = (sgn[c] >> j) & 1u;
+          const u64 e1 = ((p0 ? bit : 0ull) - a1[j]) & MN, f1 = ((p0 ? 0ull : bit) - b1[j]) & MN;
+          const u64 E = (e1 + get_word(r, j, c)) & MN;
+          const u64 F = (f1 + get_word(r, GS + j, c)) & MN;
+          const u64 tt = mul_z(p0, E, F, a1[j], b1[j], c1[j], MN);
+          d[c][j] = ((p0 ? 1ull : 0ull) - ((bit - 2 * tt) & MN)) & MN;
+        }
       }
     }
     if (!mult) {
-      store_u64s<GS>(io.y + e0, valid, d);
+#pragma unroll
+      for (int c = 0; c < C; ++c) store_u64s<GS>(io.y + e0[c], valid[c], d[c]);
       continue;
     }
     // ---- round L+2: y = MUL(x, d)
     {
       const int r = L + 2;
-      u64 e2[GS], f2[GS], yv[GS];
 #pragma unroll
-      for (int j = 0; j < GS; ++j) {
-        e2[j] = (x[j] - a2[j]) & MN;
-        f2[j] = (d[j] - b2[j]) & MN;
-        put_word(r, j, e2[j]);
-        put_word(r, GS + j, f2[j]);
+      for (int c = 0; c < C; ++c) {
+        u64 x[GS], a2[GS], b2[GS];
+        load_u64s<GS>(io.x + e0[c], valid[c], x);
+        load_u64s<GS>(io.aa + io.acur + n + e0[c], valid[c], a2);
+        load_u64s<GS>(io.ab + io.acur + n + e0[c], valid[c], b2);
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          put_word(r, j, c, (x[j] - a2[j]) & MN);
+          put_word(r, GS + j, c, (d[c][j] - b2[j]) & MN);
+        }
       }
       if (!exchange(r)) return;
 #pragma unroll
-      for (int j = 0; j < GS; ++j) {
-        const u64 E = (e2[j] + get_word(r, j)) & MN;
-        const u64 F = (f2[j] + get_word(r, GS + j)) & MN;
-        yv[j] = mul_z(p0, E, F, a2[j], b2[j], c2[j], MN);
+      for (int c = 0; c < C; ++c) {
+        u64 x[GS], a2[GS], b2[GS], c2[GS], yv[GS];
+        load_u64s<GS>(io.x + e0[c], valid[c], x);
+        load_u64s<GS>(io.aa + io.acur + n + e0[c], valid[c], a2);
+        load_u64s<GS>(io.ab + io.acur + n + e0[c], valid[c], b2);
+        load_u64s<GS>(io.ac + io.acur + n + e0[c], valid[c], c2);
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+          const u64 E = (((x[j] - a2[j]) & MN) + get_word(r, j, c)) & MN;
+          const u64 F = (((d[c][j] - b2[j]) & MN) + get_word(r, GS + j, c)) & MN;
+          yv[j] = mul_z(p0, E, F, a2[j], b2[j], c2[j], MN);
+        }
+        store_u64s<GS>(io.y + e0[c], valid[c], yv);
       }
-      store_u64s<GS>(io.y + e0, valid, yv);
     }
   }
+}
+
+template <int W, bool RING64>
+__global__ void __launch_bounds__(P2P_TP) k_relu_p2p(const P2PArgs A) {
+  p2p_party<W, RING64>(A, blockIdx.x, gridDim.x);
+}
+
+// Both parties in ONE grid on one device (CTAs [0, G) party 0, [G, 2G) party 1): the single-GPU
+// harness of the party kernel -- no dependence on two streams actually running concurrently.
+template <int W, bool RING64>
+__global__ void __launch_bounds__(P2P_TP) k_relu_p2p_dual(const P2PArgs A0, const P2PArgs A1) {
+  const unsigned g = gridDim.x / 2;
+  if (blockIdx.x < g)
+    p2p_party<W, RING64>(A0, blockIdx.x, g);
+  else
+    p2p_party<W, RING64>(A1, blockIdx.x - g, g);
 }
 
 // receive-buffer layout shared by both parties: per round, ntiles x round_bytes(r) x TP bytes
 template <int W>
 u64 p2p_layout(u64 n, int drelu_only, u64 (&off)[P2P_MAXR], u64* ntiles_out) {
   using PG = P2PGeo<W>;
-  const u64 ntiles = (n + (u64)P2P_TP * PG::GS - 1) / ((u64)P2P_TP * PG::GS);
+  const u64 chunk = (u64)P2P_TP * P2P_C * PG::GS;  // elements per chunk
+  const u64 ntiles = (n + chunk - 1) / chunk;
   const int R = PG::L + (drelu_only ? 2 : 3);
   u64 o = 0;
   for (int r = 0; r < P2P_MAXR; ++r) {
     off[r] = o;
-    if (r < R) o += ntiles * (u64)PG::round_bytes(r) * P2P_TP;
+    if (r < R) o += ntiles * (u64)PG::round_bytes(r) * P2P_TP * P2P_C;
     o = (o + 255) & ~255ull;
   }
   *ntiles_out = ntiles;
@@ -261,10 +310,17 @@ u64 p2p_layout(u64 n, int drelu_only, u64 (&off)[P2P_MAXR], u64* ntiles_out) {
 }
 
 template <int W>
-cudaError_t launch_p2p(P2PArgs A, int max_ctas, cudaStream_t s) {
+cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, cudaStream_t s) {
+  // B == nullptr: one party (A) on this device; otherwise both parties A (party 0), *B (party 1)
   u64 ntiles;
   (void)p2p_layout<W>(A.n, A.drelu_only, A.round_off, &ntiles);
   A.ntiles = ntiles;
+  P2PArgs A1;
+  if (B) {
+    A1 = *B;
+    (void)p2p_layout<W>(A1.n, A1.drelu_only, A1.round_off, &ntiles);
+    A1.ntiles = ntiles;
+  }
   if (ntiles == 0) return cudaSuccess;
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
@@ -272,21 +328,27 @@ cudaError_t launch_p2p(P2PArgs A, int max_ctas, cudaStream_t s) {
   cudaError_t e = A.N == 64 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, true>, P2P_TP, 0)
                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, false>, P2P_TP, 0);
   if (e != cudaSuccess) return e;
-  // persistent grid with residency margin: 3/4 of the co-resident CTAs when this party has the GPU
-  // to itself, 1/4 when both parties' kernels share one device (max_ctas < 0) -- a deadlock needs
-  // BOTH parties partially resident, which the margin keeps away from
+  // persistent grid with residency margin: 3/4 of the co-resident CTAs for one party on its own GPU,
+  // 3/8 per party when both share the device (a deadlock needs BOTH parties partially resident)
   const long long full = (long long)occ * sms;
-  long long grid = max_ctas < 0 ? full / 4 : (3 * full) / 4;
+  long long grid = B ? (3 * full) / 8 : (3 * full) / 4;
   if (grid < 1) grid = 1;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if ((u64)grid > ntiles) grid = (long long)ntiles;
   if (getenv("HB_P2P_DEBUG"))
-    fprintf(stderr, "[hb_relu_p2p] W=%d party=%d occ=%d/SM sms=%d grid=%lld tiles=%llu\n", W, A.party, occ, sms, grid,
-            (unsigned long long)ntiles);
-  if (A.N == 64)
-    k_relu_p2p<W, true><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
-  else
-    k_relu_p2p<W, false><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
+    fprintf(stderr, "[hb_relu_p2p] W=%d %s occ=%d/SM sms=%d grid=%lld per party, tiles=%llu\n", W,
+            B ? "both parties" : "one party", occ, sms, grid, (unsigned long long)ntiles);
+  if (B) {
+    if (A.N == 64)
+      k_relu_p2p_dual<W, true><<<(unsigned)(2 * grid), P2P_TP, 0, s>>>(A, A1);
+    else
+      k_relu_p2p_dual<W, false><<<(unsigned)(2 * grid), P2P_TP, 0, s>>>(A, A1);
+  } else {
+    if (A.N == 64)
+      k_relu_p2p<W, true><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
+    else
+      k_relu_p2p<W, false><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
+  }
   return cudaGetLastError();
 }
 

@@ -211,12 +211,55 @@ def relu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> Ar
     return _relu_staged(session, x, window, drelu_only=False)
 
 
+def relu_p2p_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitWindow, links,
+                  drelu_only: bool = False):
+    """Both parties' NVLink party kernels in one launch on this GPU (hb_relu_p2p_pair), the openings
+    going through each other's receive buffers (`links` = transport.local_p2p_pair()) exactly as
+    relu_p2p does across two GPUs.  Same shares / triples / meter as relu_pair and relu."""
+    s0, s1 = sessions
+    l0, l1 = links
+    if (s0.party, s1.party) != (0, 1) or (x0.party, x1.party) != (0, 1):
+        raise ConfigError("relu_p2p_pair expects (party 0, party 1) sessions and shares")
+    if x0.width != x1.width or x0.shape != x1.shape:
+        raise ConfigError("relu_p2p_pair shares must agree in width and shape")
+    window.check_fits(x0.width)
+    N, k, m, w = x0.width, window.k, window.m, window.width
+    a0, a1 = _flat(x0.data), _flat(x1.data)
+    n = a0.numel()
+    levels = prefix_levels(w)
+    need = {(BOOL, w): n * (1 + 2 * levels), (ARITH, N): (1 if drelu_only else 2) * n}
+    s0.triples.check(need)
+    s1.triples.check(need)
+    views = [(s.triples.draw(BOOL, w, need[(BOOL, w)]), s.triples.draw(ARITH, N, need[(ARITH, N)])) for s in sessions]
+    trace = _relu_trace(n, k, m, N, bool(drelu_only))
+    for s in sessions:
+        s.endpoint.meter.record_rounds(trace)
+    lib = _lib.load()
+    ntiles = ctypes.c_int64(0)
+    nbytes = lib.hb_relu_p2p_bytes(k, m, n, int(drelu_only), ctypes.byref(ntiles))
+    l0.check()
+    l0.ensure(nbytes, ntiles.value)
+    rounds = lib.hb_relu_rounds(k, m, int(drelu_only))
+    seq0 = l0.seq
+    l0.seq += rounds
+    l1.seq += rounds
+    y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
+    y1 = torch.empty(n, dtype=torch.int64, device=a0.device)
+    _lib.check(lib.hb_relu_p2p_pair(N, k, m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
+                                    views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),
+                                    l0.recv, l1.recv, l0.flags, l1.flags, seq0, l0.max_ctas, l0.timeout_s,
+                                    l0.err.data_ptr(), int(drelu_only), _stream()))
+    l0.after_launch(torch.cuda.current_stream())
+    return (_wrap(ArithShareTensor, 0, N, y0, x0.data, x0.shape), _wrap(ArithShareTensor, 1, N, y1, x1.data, x1.shape))
+
+
 def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, link, drelu_only: bool = False,
-             stream=None) -> ArithShareTensor:
+             stream=None, out: torch.Tensor | None = None) -> ArithShareTensor:
     """One party's ReLU / DReLU in one launch of the NVLink party kernel (hb_relu_p2p): every
     round's opening goes tile by tile into the peer's receive buffer (`link`, a transport.PeerLink)
     instead of a per-round Endpoint.exchange.  Same output shares, triple consumption and meter
-    trace as relu() over any endpoint; both parties must call it for the same layers in order."""
+    trace as relu() over any endpoint; both parties must call it for the same layers in order.
+    `out` (int64, n elements) avoids an allocation between two parties' launches on one device."""
     window.check_fits(x.width)
     N, k, m, w = x.width, window.k, window.m, window.width
     xd = _flat(x.data)
@@ -235,7 +278,9 @@ def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, l
     seq0 = link.seq
     link.seq += rounds
     session.endpoint.meter.record_rounds(_relu_trace(n, k, m, N, bool(drelu_only)))
-    y = torch.empty(n, dtype=torch.int64, device=xd.device)
+    y = torch.empty(n, dtype=torch.int64, device=xd.device) if out is None else out.reshape(-1)
+    if y.numel() != n or y.dtype != torch.int64 or not y.is_cuda:
+        raise ConfigError("relu_p2p out must be a CUDA int64 tensor of the input's size")
     st = _stream() if stream is None else stream.cuda_stream
     _lib.check(lib.hb_relu_p2p(session.party, N, k, m, n, xd.data_ptr(), y.data_ptr(), bv.abi(), av.abi(),
                                link.recv, link.flags, link.peer_recv, link.peer_flags, seq0,

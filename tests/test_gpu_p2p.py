@@ -1,9 +1,10 @@
 """GPU parity of the one-launch NVLink party kernel (hb_relu_p2p, protocol.relu_p2p).
 
 The kernel is written for one party per GPU with the peer's receive buffer mapped over NVLink.
-This run has one GPU, so the parties run as two streams of one process on the same device, each
-PeerLink pointing at the other's buffers (transport.local_p2p_pair) -- the same kernel, flags and
-fences; only the "remote" stores land in local HBM.  A second test runs the two parties as two
+This run has one GPU, so both parties' party kernels run in one launch on the same device (CTAs
+split between the parties, protocol.relu_p2p_pair), each pointing at the other's buffers
+(transport.local_p2p_pair) -- the same per-party code, flags and fences; only the "remote" stores
+land in local HBM.  A second test runs the two parties as two
 processes on the one GPU with the buffers exchanged as CUDA IPC handles (the multi-GPU plumbing).
 Bar: bit-exact per-party shares against the oracle and the fused pair kernel.
 """
@@ -28,30 +29,10 @@ from paper_2309_04875_b200.sharing import ArithShareTensor
 pytestmark = pytest.mark.gpu
 
 
-def _dev_share(t):
-    if isinstance(t.data, torch.Tensor):
-        return t, False
-    return ArithShareTensor(t.party, t.width, torch.from_numpy(np.ascontiguousarray(t.data).view(np.int64)).cuda()), True
-
-
 def _p2p_pair(s0, s1, t0, t1, win, links, drelu_only=False):
-    # inputs on the device first: a pageable host copy between the two launches would wait for
-    # party 0's kernel, which is waiting for party 1 (one device, one process)
-    (t0, host), (t1, _) = _dev_share(t0), _dev_share(t1)
-    cur = torch.cuda.current_stream()
-    st = (torch.cuda.Stream(), torch.cuda.Stream())
-    out = []
-    for s, t, lk, strm in zip((s0, s1), (t0, t1), links, st):
-        strm.wait_stream(cur)
-        with torch.cuda.stream(strm):
-            out.append(protocol.relu_p2p(s, t, win, lk, drelu_only=drelu_only, stream=strm))
-    for strm in st:
-        cur.wait_stream(strm)
-    torch.cuda.synchronize()
-    for lk in links:
-        lk.check(sync=True)
-    if host:
-        out = [ArithShareTensor(o.party, o.width, o.data.cpu().numpy().view(np.uint64)) for o in out]
+    links[0].timeout_s = 20.0
+    out = protocol.relu_p2p_pair((s0, s1), t0, t1, win, links, drelu_only=drelu_only)
+    links[0].check(sync=True)
     return out
 
 
@@ -107,7 +88,8 @@ def test_p2p_sequence_growth_and_large():
 
 
 def test_p2p_missing_peer_times_out():
-    """Only party 0 runs: its kernel gives up after the timeout and the link raises."""
+    """Only party 0 runs (relu_p2p, one party): its kernel gives up after the timeout and the
+    link raises instead of hanging."""
     links = transport.local_p2p_pair()
     links[0].timeout_s = 0.05
     n = 4096

@@ -179,6 +179,9 @@ def _dist_worker(rank, port, q):
     with ep.tag("Circuit"):
         for i in range(3):
             got.append(ep.exchange(bytes([rank]) * (8 * (i + 1))))
+    # no CUDA here: the NVLink party path cannot map the peer, both ranks agree to stay staged
+    p2p = ep.enable_p2p(timeout_s=1.0)
+    got.append(p2p is None and ep.p2p is None)
     q.put((rank, got, ep.meter.to_json()))
     dist.destroy_process_group()
 
@@ -195,8 +198,8 @@ def test_dist_endpoint_gloo_world2():
     res = dict((r, (g, m)) for r, g, m in (q.get(timeout=120) for _ in ps))
     for p in ps:
         p.join(60)
-    assert res[0][0] == [bytes([1]) * 8, bytes([1]) * 16, bytes([1]) * 24]
-    assert res[1][0] == [bytes([0]) * 8, bytes([0]) * 16, bytes([0]) * 24]
+    assert res[0][0] == [bytes([1]) * 8, bytes([1]) * 16, bytes([1]) * 24, True]
+    assert res[1][0] == [bytes([0]) * 8, bytes([0]) * 16, bytes([0]) * 24, True]
     assert res[0][1]["tags"]["Circuit"] == {"bytes": 48, "rounds": 3}
 
 
