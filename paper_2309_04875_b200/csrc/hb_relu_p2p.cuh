@@ -69,6 +69,12 @@ HB_DEV unsigned long long ld_acquire_sys(const unsigned long long* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+HB_DEV unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+HB_DEV void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 HB_DEV unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -138,17 +144,21 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
     auto exchange = [&](int r) -> bool {  // release round r of this chunk, acquire the peer's
       __syncthreads();
       if (t == 0) {
+        // the CTA's stores to the peer are ordered before this thread by the barrier; the release
+        // store is cumulative over them at system scope
         const unsigned long long seq = A.seq0 + (u64)r + 1;
-        __threadfence_system();
         st_release_sys(A.peer_flag + tile, seq);
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire_sys(A.my_flag + tile) < seq) {
-          if (globaltimer() - t0 > A.timeout_ns) {
-            atomicExch(A.err, 1);
-            abort_s = 1;
-            break;
+        if (ld_relaxed_sys(A.my_flag + tile) < seq) {
+          const unsigned long long t0 = globaltimer();
+          while (ld_relaxed_sys(A.my_flag + tile) < seq) {
+            if (globaltimer() - t0 > A.timeout_ns) {
+              atomicExch(A.err, 1);
+              abort_s = 1;
+              break;
+            }
           }
         }
+        fence_acq_rel_sys();  // acquire: the peer's stores are visible before the barrier releases the CTA
       }
       __syncthreads();
       return abort_s == 0;
