@@ -53,6 +53,8 @@ def parse():
                    help="N=1 driver: fused pair kernel, staged rounds, or the P2P party kernels on two streams")
     p.add_argument("--multi-path", choices=["p2p", "nccl"], default="p2p",
                    help="N>1: one-launch NVLink party kernel (peer buffers over CUDA IPC) or staged rounds + NCCL")
+    p.add_argument("--graph", action="store_true",
+                   help="capture the timed steps in one CUDA graph (no host launch overhead; small layers)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-resnet", action="store_true", help="skip the ResNet18 secondary measurement")
@@ -235,19 +237,31 @@ def run_single(args):
         y0, y1 = step(x0, x1)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    graph = None
+    if args.graph:  # the timed steps as one CUDA graph: what the GPU sustains without host launch gaps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(args.steps):
+                y0, y1 = step(x0, x1)
+        graph.replay()  # warm
+        torch.cuda.synchronize()
     with ClockSampler(0) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t_start.record(s)
-        for i in range(args.steps):
-            ev[i][0].record(s)
-            y0, y1 = step(x0, x1)
-            ev[i][1].record(s)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                ev[i][0].record(s)
+                y0, y1 = step(x0, x1)
+                ev[i][1].record(s)
         t_end.record(s)
         torch.cuda.synchronize()
     total_ms = t_start.elapsed_time(t_end)
-    launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    launch_ms = (total_ms / args.steps if graph is not None
+                 else statistics.mean(a.elapsed_time(b) for a, b in ev))
     ok = check_sample(x0, x1, y0.data, y1.data, N, k, m)
     value = n * args.steps / (total_ms / 1e3)
 
@@ -315,6 +329,7 @@ def run_single(args):
                                    "each other's receive buffers"}[args.path],
                    "inputs": "x_f~N(0,4^2), f=16, additive shares; Beaver triples from the on-device dealer",
                    "triple_sets": sets, "l2": f"inputs {2 * n * bpe['fused'] / 1e9:.2f} GB/step > 126 MB L2",
+                   "cuda_graph": bool(args.graph),
                    "parallelism": "pair"},
         "correct": ok,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -671,11 +686,12 @@ def run_sweep(args):
         for k, m in ((64, 0), (32, 0), (22, 6), (22, 14), (22, 16)):
             a = copy.copy(args)
             a.logn, a.k, a.m = logn, k, m
-            a.no_e2e, a.no_cpu_baseline = True, True
+            a.no_e2e, a.no_cpu_baseline, a.no_resnet = True, True, True
+            a.graph = logn <= 22  # small layers: launch gaps would dominate the GPU time
             a.steps = max(5, min(args.steps, 20))
             a.warmup = 3
             r = run_single(a)
-            row = {"logn": logn, "k": k, "m": m, "w": k - m, "elems_per_s": r["value"],
+            row = {"logn": logn, "k": k, "m": m, "w": k - m, "cuda_graph": a.graph, "elems_per_s": r["value"],
                    "ms_per_step": r["ms_per_step"], "hbm_frac": r["roofline"]["frac"],
                    "frac_vs_survey_H": r["roofline"]["frac_vs_survey_H"], "correct": r["correct"]}
             log(json.dumps(row))
