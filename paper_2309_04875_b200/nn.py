@@ -649,11 +649,14 @@ def build_stores(model: ModelSpec, relu_cfg: ReluConfig, batch: int, seed: int):
     return stores
 
 
-def run_local_forward(model: ModelSpec, relu_cfg: ReluConfig, x_f, seed: int, pair: bool = True):
+def run_local_forward(model: ModelSpec, relu_cfg: ReluConfig, x_f, seed: int, pair: bool = True,
+                      layer_logs: bool = True):
     """Both parties in process -> (logits, (meter0, meter1), layer_logs, wall_ms) (cli.py:159-180).
 
     pair=True runs the parties time-sliced on this GPU (fused ReLU kernel);
-    pair=False runs two party threads over a LocalEndpoint, as the reference does."""
+    pair=False runs two party threads over a LocalEndpoint, as the reference does.
+    layer_logs=False skips the per-layer meter log (empty logs), which lets the runner fuse a
+    residual block's add into its last conv."""
     cfg = model.fixed_point
     enc = ring.encode_array(x_f, cfg)
     s0, s1 = sharing.share_arith(enc, cfg.ring_bits, _seed_rng(seed, _INPUT_STREAM))
@@ -661,13 +664,14 @@ def run_local_forward(model: ModelSpec, relu_cfg: ReluConfig, x_f, seed: int, pa
     ep0, ep1 = transport.local_pair()
     sessions = (ProtocolSession(ep0, stores[0], cfg), ProtocolSession(ep1, stores[1], cfg))
     logs: tuple = ([], [])
+    lg = logs if layer_logs else (None, None)
     torch.cuda.synchronize()
     start = time.perf_counter()
     if pair:
-        o0, o1 = model_forward_pair(sessions, s0, s1, model, relu_cfg, logs)
+        o0, o1 = model_forward_pair(sessions, s0, s1, model, relu_cfg, lg if layer_logs else None)
     else:
-        o0, o1 = transport.run_parties(lambda: model_forward(sessions[0], s0, model, relu_cfg, logs[0]),
-                                       lambda: model_forward(sessions[1], s1, model, relu_cfg, logs[1]),
+        o0, o1 = transport.run_parties(lambda: model_forward(sessions[0], s0, model, relu_cfg, lg[0]),
+                                       lambda: model_forward(sessions[1], s1, model, relu_cfg, lg[1]),
                                        endpoints=(ep0, ep1))
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - start) * 1e3

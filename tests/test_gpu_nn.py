@@ -88,6 +88,38 @@ def test_resnet_shaped_vs_oracle(windows):
         assert [tuple(t) for t in meters[0].trace] == [tuple(t) for t in traces[0]]
 
 
+def _wide_resnet():
+    """ResNet-shaped, wide enough (>= 64 channels) for the TMA conv kernels: the 3-channel stem on
+    the gather kernel, a basic block on k_conv_tma<64,1,..> with the residual add fused into its
+    epilogue, a strided block on the two-pass N_T=128 kernel with a 1x1 strided shortcut, and the
+    linear layer as a 1x1 conv (N_T=16)."""
+    ini = models._Init(4)
+    layers = [ini.conv("stem", 3, 64, 3, 1, 1), nn.Relu(0)]
+    layers += models._basic_block(ini, "b1", 64, 64, 1, 1)
+    layers += models._basic_block(ini, "b2", 64, 128, 2, 2)
+    layers += [nn.AvgPool(4, 4, 4), nn.Flatten(), ini.linear("fc", 128, 10)]
+    return nn.ModelSpec(FixedPointConfig(), (3, 8, 8), layers, ini.weights)
+
+
+@pytest.mark.parametrize("pair", [True, False], ids=["pair", "threads"])
+def test_wide_resnet_tma_fused_vs_oracle(pair):
+    """Model-level parity through the TMA convs with the fused residual adds (no layer log):
+    logits equal the oracle's run_local_forward exactly (batch 3: a partial TMA box)."""
+    model = _wide_resnet()
+    windows = [(22, 14), (64, 0), (20, 6)]
+    x_f = np.random.default_rng(8).uniform(0, 1, (3, 3, 8, 8))
+    cfg = nn.ReluConfig([BitWindow(*w) for w in windows])
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    want, traces, _ = ON.run_local_forward(layers, model.input_shape, model.weights, windows, x_f, 11)
+    logits, meters, logs, _ = nn.run_local_forward(model, cfg, x_f, 11, pair=pair, layer_logs=False)
+    assert np.array_equal(logits, want)
+    assert [tuple(t) for t in meters[0].trace] == [tuple(t) for t in traces[0]]
+    assert logs == ([], [])
+    # and with the per-layer log (unfused adds) the same logits
+    logits2, _, logs2, _ = nn.run_local_forward(model, cfg, x_f, 11, pair=pair)
+    assert np.array_equal(logits2, want) and len(logs2[0]) > 0
+
+
 def test_resnet18_forward_smoke():
     """Full ResNet18-CIFAR at batch 2: runs, spends the analytic rounds, and the logits
     track the plaintext fixed-point forward (fidelity, not exactness: local truncation)."""
