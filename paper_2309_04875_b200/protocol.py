@@ -344,13 +344,14 @@ def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitW
 _PIPE: dict = {}
 
 
-def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=1 << 21):
-    """Pinned host shares in/out: the layer goes through in chunks on three streams so the
+def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=1 << 21, nstreams=3):
+    """Pinned host shares in/out: the layer goes through in chunks on `nstreams` streams so the
     H2D copy of chunk c+1, the fused kernel on chunk c and the D2H copy of chunk c-1 overlap
-    (PCIe is full duplex).  Same kernel, same triples, same shares as the one-shot path."""
+    (PCIe is full duplex; small chunks keep the pipeline fill / drain short).  Same kernel, same
+    triples, same shares as the one-shot path."""
     dev = _dev.device()
     if dev.index not in _PIPE:
-        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(3))
+        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(nstreams))
     streams = _PIPE[dev.index]
     h0, h1 = x0.data.reshape(-1), x1.data.reshape(-1)
     d0, d1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
@@ -358,17 +359,17 @@ def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=1 << 21):
     o0, o1 = torch.empty(n, dtype=torch.int64, pin_memory=True), torch.empty(n, dtype=torch.int64, pin_memory=True)
     cur = torch.cuda.current_stream()
     lib = _lib.load()
+    tv = (views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi())  # same for every chunk
+    fn = lib.hb_relu_pair_range
     for c, lo in enumerate(range(0, n, chunk)):
         hi = min(n, lo + chunk)
-        st = streams[c % 3]
+        st = streams[c % len(streams)]
         st.wait_stream(cur)
         with torch.cuda.stream(st):
             d0[lo:hi].copy_(h0[lo:hi], non_blocking=True)
             d1[lo:hi].copy_(h1[lo:hi], non_blocking=True)
-            _lib.check(lib.hb_relu_pair_range(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(),
-                                              e0.data_ptr(), e1.data_ptr(), views[0][0].abi(), views[1][0].abi(),
-                                              views[0][1].abi(), views[1][1].abi(), int(drelu_only),
-                                              st.cuda_stream))
+            _lib.check(fn(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(), e0.data_ptr(),
+                          e1.data_ptr(), *tv, int(drelu_only), st.cuda_stream))
             o0[lo:hi].copy_(e0[lo:hi], non_blocking=True)
             o1[lo:hi].copy_(e1[lo:hi], non_blocking=True)
     for st in streams:
