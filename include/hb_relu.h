@@ -207,6 +207,14 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
                      int pad, const int8_t* wlimbs, int n_out, int j_limbs, int64_t k_padded, int n_tile, int party,
                      int frac_bits, const uint64_t* bias, uint64_t* y, void* stream);
 
+/* Simulator ReLU in the clear (simulator.py:47-54 sim_relu, the window search's inner loop):
+ * encode x * 2^frac_bits (ring.py:191-199), split with r = the raw PCG64 stream whose 128-bit
+ * (state, inc) the caller's numpy generator holds before the draw (share_arith, sharing.py:88-96),
+ * keep x iff drelu_from_shares (simulator.py:33-44) on [m, k) says so; out = x * keep in float64,
+ * bit-identical to the reference.  *err_dev = 1 if an input leaves the signed ring (EncodeRangeError). */
+int hb_sim_relu(const double* x, int64_t n, int frac_bits, int ring_bits, int k, int m, uint64_t state_lo,
+                uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, double* out, int* err_dev, void* stream);
+
 /* Byte-limb planes of an NCHW share for the TMA conv, channel-blocked NHWC:
  * planes[i][c/64][b][h][w][c%64] = byte i of x[b][c][h][w] (uint8; channels % 64 == 0;
  * 8 planes of batch*height*width*channels bytes).

@@ -15,6 +15,10 @@
 #include "hb_ring_tc.cuh"
 #include "hb_conv_tma.cuh"
 
+cudaError_t hb_sim_relu_launch(const double* x, unsigned long long n, double scale, int ring_bits, int k, int m,
+                               uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, double* out, int* err,
+                               cudaStream_t s);
+
 using hb::u64;
 
 // ---- per-range dispatchers (hb_relu_w*.cu)
@@ -565,6 +569,16 @@ int hb_conv_limbs_tc(const uint64_t* x, int batch, int channels, int height, int
   A.y = y;
   if (A.M == 0) return HB_OK;
   return cuda_status(hb_tc_conv(A, n_tile, S(stream)), "hb_conv_limbs_tc");
+}
+
+int hb_sim_relu(const double* x, int64_t n, int frac_bits, int ring_bits, int k, int m, uint64_t state_lo,
+                uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, double* out, int* err_dev, void* stream) {
+  int rc = check_window(ring_bits, k, m);
+  if (rc) return rc;
+  if (n < 0 || frac_bits < 0 || frac_bits >= ring_bits) return fail(HB_ERR_CONFIG, "bad sim_relu arguments");
+  return cuda_status(hb_sim_relu_launch(x, (unsigned long long)n, ldexp(1.0, frac_bits), ring_bits, k, m, state_lo,
+                                        state_hi, inc_lo, inc_hi, out, err_dev, S(stream)),
+                     "hb_sim_relu");
 }
 
 int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int width, uint8_t* planes, void* stream) {

@@ -88,8 +88,50 @@ __global__ void k_deal(uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_h
   }
 }
 
+// Simulator ReLU (ringmpc simulator.py:47-54 sim_relu): encode x * 2^f round-half-away-from-zero
+// onto Z/2^N (ring.py:191-199), split with r = raw PCG64 outputs of the caller's generator
+// (rng.bytes, ring.py:207-213; share_arith sharing.py:88-96), decide on the window [m, k)
+// (drelu_from_shares simulator.py:33-44) and keep-or-zero in float64 -- x * 1.0 / x * 0.0, the
+// reference's arithmetic, so the output is bit-identical.
+__global__ void k_sim_relu(const double* __restrict__ x, unsigned long long n, double scale, int ring_bits, int k,
+                           int m, uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, double* __restrict__ out,
+                           int* __restrict__ err) {
+  const unsigned long long e0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * RUN;
+  if (e0 >= n) return;
+  const u128 M = mk(0x4385DF649FCCF645ull, 0x2360ED051FC65DA4ull);
+  const u128 inc = mk(i_lo, i_hi);
+  u128 st = advance(mk(s_lo, s_hi), M, inc, e0);
+  const uint64_t mask = ring_bits >= 64 ? ~0ull : ((1ull << ring_bits) - 1);
+  const int w = k - m;
+  const uint64_t wmask = w >= 64 ? ~0ull : ((1ull << w) - 1);
+  const double half = ldexp(1.0, ring_bits - 1);
+  const unsigned long long end = e0 + RUN < n ? e0 + RUN : n;
+  for (unsigned long long i = e0; i < end; ++i) {
+    st = st * M + inc;
+    const uint64_t r = xsl_rr(st) & mask;
+    const double v = x[i], sc = v * scale;
+    const double rd = copysign(floor(fabs(sc) + 0.5), sc);
+    if (fabs(rd) >= half) atomicExch(err, 1);  // EncodeRangeError
+    const uint64_t enc = (uint64_t)(long long)rd & mask;
+    const uint64_t s0 = (enc + r) & mask, s1 = (0ull - r) & mask;
+    const uint64_t t = (((s0 >> m) & wmask) + ((s1 >> m) & wmask)) & wmask;
+    const double keep = (double)(1ull - ((t >> (w - 1)) & 1ull));
+    out[i] = v * keep;
+  }
+}
+
 }  // namespace dealer
 }  // namespace hb
+
+cudaError_t hb_sim_relu_launch(const double* x, unsigned long long n, double scale, int ring_bits, int k, int m,
+                               uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, double* out, int* err,
+                               cudaStream_t s) {
+  const unsigned long long runs = (n + hb::dealer::RUN - 1) / hb::dealer::RUN;
+  if (runs)
+    hb::dealer::k_sim_relu<<<(unsigned)((runs + 127) / 128), 128, 0, s>>>(x, n, scale, ring_bits, k, m, s_lo, s_hi,
+                                                                          i_lo, i_hi, out, err);
+  return cudaGetLastError();
+}
 
 cudaError_t hb_dealer_launch(uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, int kind, int width,
                              unsigned long long count, unsigned long long first, unsigned long long n, uint64_t* a0,

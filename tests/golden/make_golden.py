@@ -17,7 +17,9 @@ bit-for-bit by numpy alone (see tests/golden_cases.py):
 * stage kernels: beaver_mul/beaver_and/circuit_add/a2b/b2a_bit
   (test_protocol.py:110-271);
 * pack layouts for w = 1..64 (test_transport.py:22-48);
-* dealer streams and the HBTRIP1 golden SHA (test_dealer.py:14,82-86).
+* dealer streams and the HBTRIP1 golden SHA (test_dealer.py:14,82-86);
+* the simulator: sim_relu outputs, sim_forward / plain_forward logits, DReLU masks and
+  activation ranges on the desk models (simulator.py:33-174).
 """
 
 from __future__ import annotations
@@ -237,6 +239,29 @@ def main():
                             "meter0": meters[0].to_json(), "meter1": meters[1].to_json(),
                             "layers0": logs[0], "layers1": logs[1]}
         ARR[mc["name"] + "/logits"] = logits
+
+    # ---------------- simulator (simulator.py:33-174): sim_relu, sim_forward, plain_forward, ranges
+    from ringmpc import simulator as sim
+
+    for case in gc.SIM_RELU_CASES:
+        x = gc.sim_relu_input(case)
+        rng = np.random.default_rng(np.random.SeedSequence(case["split_seed"]))
+        out = sim.sim_relu(x, BitWindow(case["k"], case["m"]), FixedPointConfig(64, 16), rng)
+        ARR[case["name"] + "/out"] = out
+        META[case["name"]] = {"out_sha": sha(np.ascontiguousarray(out).view(np.uint64))}
+    for mc in gc.SIM_MODEL_CASES:
+        model = models.build_cnn(11) if mc["arch"] == "cnn" else models.build_mlp(11)
+        x_f, labels = gc.sim_model_inputs(mc)
+        cfg = sim.SimConfig(FixedPointConfig(64, 16), [None if w is None else BitWindow(*w) for w in mc["windows"]],
+                            seed=mc["seed"])
+        logits, acc = sim.sim_forward(model, x_f, labels, cfg)
+        _, masks = sim.collect_drelu_decisions(model, x_f, cfg)
+        ARR[mc["name"] + "/logits"] = logits
+        ARR[mc["name"] + "/plain"] = sim.plain_forward(model, x_f)
+        for i, mk in enumerate(masks):
+            ARR[mc["name"] + f"/mask{i}"] = mk
+        META[mc["name"]] = {"accuracy": acc, "n_masks": len(masks),
+                            "ranges": {str(g): v for g, v in sim.collect_activation_ranges(model, x_f).items()}}
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **ARR)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:

@@ -262,3 +262,27 @@ MODEL_LAYERS = {
 def model_weights(arrays, arch):
     pre = f"model_{arch}/"
     return {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
+
+
+# ---------------------------------------------------------------- simulator (simulator.py:33-174)
+SIM_RELU_CASES = [
+    dict(name="simrelu_22_14", k=22, m=14, n=20000, seed=31, split_seed=[9, 2]),
+    dict(name="simrelu_64_0", k=64, m=0, n=5001, seed=32, split_seed=[9, 3]),
+    dict(name="simrelu_20_6", k=20, m=6, n=7777, seed=33, split_seed=[4, 1]),
+]
+
+SIM_MODEL_CASES = [
+    dict(name="sim_cnn_reduced", arch="cnn", windows=[(20, 8), (19, 6)], seed=3, batch=16),
+    dict(name="sim_cnn_mixed", arch="cnn", windows=[None, (22, 14)], seed=5, batch=16),
+    dict(name="sim_mlp_reduced", arch="mlp", windows=[(21, 13)], seed=7, batch=32),
+]
+
+
+def sim_relu_input(case):
+    return np.random.default_rng(case["seed"]).normal(0.0, 4.0, case["n"])
+
+
+def sim_model_inputs(mc):
+    rng = np.random.default_rng(91 + mc["batch"])
+    shape = (mc["batch"], 1, 8, 8) if mc["arch"] == "cnn" else (mc["batch"], 64)
+    return rng.uniform(0.0, 1.0, shape), rng.integers(0, 10, mc["batch"])

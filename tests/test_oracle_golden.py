@@ -174,3 +174,32 @@ def test_model_run_local_forward(golden, mc):
     assert logs[0] == g["layers0"] and logs[1] == g["layers1"]
     tot = O.tag_totals(traces[0])
     assert {t: {"bytes": tot[t][0], "rounds": tot[t][1]} for t in O.TAGS} == g["meter0"]["tags"]
+
+
+# ---------------------------------------------------------------- simulator (simulator.py:33-174)
+from oracle import hb_oracle_sim as OS  # noqa: E402
+
+
+@pytest.mark.parametrize("case", gc.SIM_RELU_CASES, ids=[c["name"] for c in gc.SIM_RELU_CASES])
+def test_sim_relu_oracle(golden, case):
+    meta, arrays = golden
+    rng = np.random.default_rng(np.random.SeedSequence(case["split_seed"]))
+    out = OS.sim_relu(gc.sim_relu_input(case), case["k"], case["m"], rng)
+    assert np.array_equal(out.view(np.uint64), arrays[case["name"] + "/out"].view(np.uint64))
+
+
+@pytest.mark.parametrize("mc", gc.SIM_MODEL_CASES, ids=[c["name"] for c in gc.SIM_MODEL_CASES])
+def test_sim_forward_oracle(golden, mc):
+    meta, arrays = golden
+    g = meta[mc["name"]]
+    layers, _ = gc.MODEL_LAYERS[mc["arch"]]
+    weights = gc.model_weights(arrays, mc["arch"])
+    x_f, labels = gc.sim_model_inputs(mc)
+    logits, acc = OS.sim_forward(layers, weights, x_f, labels, mc["windows"], mc["seed"])
+    assert np.array_equal(logits, arrays[mc["name"] + "/logits"]) and acc == g["accuracy"]
+    _, masks = OS.collect_drelu_decisions(layers, weights, x_f, mc["windows"], mc["seed"])
+    assert len(masks) == g["n_masks"]
+    for i, mk in enumerate(masks):
+        assert np.array_equal(mk, arrays[mc["name"] + f"/mask{i}"])
+    assert np.array_equal(OS.plain_forward(layers, weights, x_f), arrays[mc["name"] + "/plain"])
+    assert {str(k): v for k, v in OS.collect_activation_ranges(layers, weights, x_f).items()} == g["ranges"]
