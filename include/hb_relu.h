@@ -221,6 +221,12 @@ int hb_sim_relu(const double* x, int64_t n, int frac_bits, int ring_bits, int k,
  * Replaces the limb split inside the reference's uint64 matmul (nn.py:222). */
 int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int width, uint8_t* planes, void* stream);
 
+/* Small-K convs (channels*kh*kw <= 64, e.g. a 3-channel stem): the byte-limb planes of the im2col
+ * patches, [limb][1][batch][OH][OW][64] with patch index c*kh*kw + ki*kw + kj (nn.py:177-195) zero-
+ * padded to 64 -- the conv then runs through hb_conv_limbs_tma as a 1x1 conv over 64 channels. */
+int hb_im2col_planes(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                     int pad, uint8_t* planes, void* stream);
+
 /* Ring conv/linear (nn.py:214-243 conv2d_forward / linear_forward + truncate_local nn.py:198-211) as a
  * TMA-fed tcgen05 implicit GEMM over the limb planes of hb_limbs_nhwc: same result as
  * hb_conv_limbs_tc.  wlimbs: int8 [ceil(n_out/n_tile)][kh*kw*channels/64][j_limbs][n_tile x 64

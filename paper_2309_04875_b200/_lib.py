@@ -110,6 +110,7 @@ _SIGS = {
     "hb_sim_relu": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "hb_im2col_planes": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p, ctypes.c_void_p]),
     "hb_limbs_nhwc": (ctypes.c_int, [u64p] + [ctypes.c_int] * 4 + [u64p, ctypes.c_void_p]),
     "hb_conv_limbs_tma": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p] + [ctypes.c_int] * 5 + [u64p, u64p, u64p,
                                                                                                  ctypes.c_void_p]),

@@ -588,6 +588,16 @@ int hb_limbs_nhwc(const uint64_t* x, int batch, int channels, int height, int wi
                      "hb_limbs_nhwc");
 }
 
+int hb_im2col_planes(const uint64_t* x, int batch, int channels, int height, int width, int kh, int kw, int stride,
+                     int pad, uint8_t* planes, void* stream) {
+  if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
+    return fail(HB_ERR_CONFIG, "bad conv geometry");
+  if (channels * kh * kw > 64) return fail(HB_ERR_CONFIG, "im2col planes need C*kh*kw <= 64");
+  if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
+  return cuda_status(hb_im2col_planes_launch(x, batch, channels, height, width, kh, kw, stride, pad, planes, S(stream)),
+                     "hb_im2col_planes");
+}
+
 int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
                       int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
                       int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream) {

@@ -95,6 +95,49 @@ __global__ void __launch_bounds__(256) k_limbs_nhwc(const u64* __restrict__ x, l
   }
 }
 
+// k_im2col_planes  small-K convs (C*kh*kw <= 64, e.g. the 3-channel stem): the 8 byte-limb planes
+//                  of the im2col patches themselves, [limb][1][B][OH][OW][64] with patch index
+//                  k = c*kh*kw + ki*kw + kj (the reference order, nn.py:177-195) zero-padded to 64,
+//                  so the conv runs as a 1x1 conv with 64 channels on the TMA kernel.  Thread =
+//                  (output pixel, 8 patch entries): 8 gathers (the input is tiny and L2-resident), an
+//                  8x8 byte transpose, one 8-byte store per limb (64-byte rows, coalesced).
+__global__ void __launch_bounds__(256) k_im2col_planes(const u64* __restrict__ x, int B, int C, int H, int W, int kh,
+                                                       int kw, int stride, int pad, int OH, int OW,
+                                                       uint8_t* __restrict__ planes) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long P = (long long)B * OH * OW;
+  const int g = (int)(idx & 7);
+  const long long q = idx >> 3;  // output pixel
+  if (q >= P) return;
+  const int b = (int)(q / ((long long)OH * OW)), rem = (int)(q - (long long)b * OH * OW);
+  const int oh = rem / OW, ow = rem - (rem / OW) * OW;
+  const int K = C * kh * kw, khw = kh * kw;
+  u64 v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int k = g * 8 + e;
+    v[e] = 0;
+    if (k < K) {
+      const int c = k / khw, t = k - c * khw, ki = t / kw, kj = t - (t / kw) * kw;
+      const int ih = oh * stride - pad + ki, iw = ow * stride - pad + kj;
+      if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W)
+        v[e] = (u64)__ldg(reinterpret_cast<const unsigned long long*>(x + (((long long)b * C + c) * H + ih) * W + iw));
+    }
+  }
+  uint32_t lo03[4], lo47[4], hi03[4], hi47[4];
+  bytes_t4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3], lo03);
+  bytes_t4((uint32_t)v[4], (uint32_t)v[5], (uint32_t)v[6], (uint32_t)v[7], lo47);
+  bytes_t4((uint32_t)(v[0] >> 32), (uint32_t)(v[1] >> 32), (uint32_t)(v[2] >> 32), (uint32_t)(v[3] >> 32), hi03);
+  bytes_t4((uint32_t)(v[4] >> 32), (uint32_t)(v[5] >> 32), (uint32_t)(v[6] >> 32), (uint32_t)(v[7] >> 32), hi47);
+  uint8_t* dst = planes + q * 64 + g * 8;
+  const long long plane = P * 64;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    *reinterpret_cast<uint2*>(dst + i * plane) = make_uint2(lo03[i], lo47[i]);
+    *reinterpret_cast<uint2*>(dst + (4 + i) * plane) = make_uint2(hi03[i], hi47[i]);
+  }
+}
+
 // ------------------------------------------------------------------ implicit-GEMM conv
 
 constexpr int TKB = 64;                            // K bytes (channels) per pipeline stage = 2 MMA K steps
@@ -513,6 +556,16 @@ cudaError_t hb_limbs_nhwc_launch(const uint64_t* x, long long B, int C, long lon
   const long long tiles = B * ((HW + hb::tc::LP_P - 1) / hb::tc::LP_P);
   dim3 grid((unsigned)tiles, (unsigned)((C + hb::tc::LP_C - 1) / hb::tc::LP_C));
   hb::tc::k_limbs_nhwc<<<grid, 256, 0, s>>>(x, B, C, (int)HW, planes);
+  return cudaGetLastError();
+}
+
+cudaError_t hb_im2col_planes_launch(const uint64_t* x, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
+                                    uint8_t* planes, cudaStream_t s) {
+  const int OH = (H + 2 * pad - kh) / stride + 1, OW = (W + 2 * pad - kw) / stride + 1;
+  const long long threads = (long long)B * OH * OW * 8;
+  if (threads == 0) return cudaSuccess;
+  hb::tc::k_im2col_planes<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(x, B, C, H, W, kh, kw, stride, pad, OH,
+                                                                              OW, planes);
   return cudaGetLastError();
 }
 

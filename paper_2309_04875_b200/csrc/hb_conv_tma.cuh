@@ -29,6 +29,8 @@ struct TmaConvArgs {
 
 cudaError_t hb_limbs_nhwc_launch(const uint64_t* x, long long B, int C, long long HW, uint8_t* planes,
                                  cudaStream_t s);
+cudaError_t hb_im2col_planes_launch(const uint64_t* x, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
+                                    uint8_t* planes, cudaStream_t s);
 int hb_tma_conv_box(int B, int OH, int OW, int* bb, int* bh, int* bw);
 cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
                         const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias,

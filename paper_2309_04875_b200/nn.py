@@ -229,6 +229,7 @@ class _LimbWeight:
     nt: int = 0
     wl_tma: torch.Tensor | None = None  # int8 tiles for hb_conv_limbs_tma, K order (ki, kj, c)
     nt_tma: int = 0                     # its N tile: 128 (two shift passes) when n >= 128
+    wl_i2c: torch.Tensor | None = None  # small-K convs: im2col-plane tiles (K = C*kh*kw <= 64 padded to 64)
 
 
 def _balanced_limbs(w: np.ndarray):
@@ -277,6 +278,9 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
                 limbs_t = limbs
             lw.nt_tma = 128 if n >= 128 and _TMA_WIDE else lw.nt
             lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt_tma, k, TMA_KB)).to(dev)
+        elif w.ndim == 4 and k <= TMA_KB:  # small K: 1x1 conv over the im2col planes (reference K order)
+            lw.nt_tma = 128 if n >= 128 and _TMA_WIDE else lw.nt
+            lw.wl_i2c = torch.from_numpy(_tc_tiles(limbs, n, k, lw.nt_tma, TMA_KB, TMA_KB)).to(dev)
     return lw
 
 
@@ -380,6 +384,13 @@ def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int,
         _lib.call("hb_conv_limbs_tma", planes.data_ptr(), b, c, h, w, kh, kw, stride, pad, lw.wl_tma.data_ptr(),
                   lw.n, lw.j, lw.nt_tma, party, frac, lw.bias.data_ptr() if party == 0 else None,
                   None if residual is None else residual.contiguous().data_ptr(), out.data_ptr(), s)
+        return out
+    if RING_GEMM == "tc" and lw.wl_i2c is not None and b > 0 and _tma_box_ok(oh, ow) and residual is None:
+        s = _dev.stream_handle()
+        planes = torch.empty(8 * b * oh * ow * TMA_KB, dtype=torch.uint8, device=x_nchw.device)
+        _lib.call("hb_im2col_planes", x_nchw.data_ptr(), b, c, h, w, kh, kw, stride, pad, planes.data_ptr(), s)
+        _lib.call("hb_conv_limbs_tma", planes.data_ptr(), b, TMA_KB, oh, ow, 1, 1, 1, 0, lw.wl_i2c.data_ptr(), lw.n,
+                  lw.j, lw.nt_tma, party, frac, lw.bias.data_ptr() if party == 0 else None, None, out.data_ptr(), s)
         return out
     if residual is not None:
         raise ConfigError("residual fusion needs the TMA conv path")
