@@ -276,7 +276,9 @@ def _prep_weight(weight: np.ndarray, bias: np.ndarray, cfg: FixedPointConfig) ->
                 limbs_t = [l.reshape(n, c, kh, kw).transpose(0, 2, 3, 1).reshape(n, k) for l in limbs]
             else:
                 limbs_t = limbs
-            lw.nt_tma = 128 if n >= 128 and _TMA_WIDE else lw.nt
+            # two shift passes (N tile 128) pay off when the K loop is long enough to amortise the
+            # second TMEM drain per tile; short-K convs (ResNet 1x1s) stay on one pass at N tile 64
+            lw.nt_tma = 128 if n >= 128 and _TMA_WIDE and k >= _TMA_WIDE_MIN_K else lw.nt
             lw.wl_tma = torch.from_numpy(_tc_tiles(limbs_t, n, k, lw.nt_tma, k, TMA_KB)).to(dev)
         elif w.ndim == 4 and k <= TMA_KB:  # small K: 1x1 conv over the im2col planes (reference K order)
             lw.nt_tma = 128 if n >= 128 and _TMA_WIDE else lw.nt
@@ -305,6 +307,7 @@ def _tc_tiles(limbs, n, k, nt, kp, kb=64):
 
 TMA_KB = 64  # channel bytes per stage of hb_conv_limbs_tma (hb_conv_tma.cu TKB)
 _TMA_WIDE = os.environ.get("HB_TMA_NT", "128") != "64"  # N tile 128 (two passes) for n >= 128
+_TMA_WIDE_MIN_K = int(os.environ.get("HB_TMA_WIDE_MIN_K", "512"))
 
 
 _WCACHE: dict = {}
