@@ -605,7 +605,10 @@ def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_me
                     layer_meter[p].append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
         return ds, lay
 
-    ds, lay = run(model.layers, datas, "nchw" if datas[0].dim() == 4 else "flat", "")
+    try:
+        ds, lay = run(model.layers, datas, "nchw" if datas[0].dim() == 4 else "flat", "")
+    finally:
+        _PLANES.clear()  # the limb-plane cache only serves convs sharing an input within one forward
     return [_to_layout(d, lay, "nchw") for d in ds]
 
 
