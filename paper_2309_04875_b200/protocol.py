@@ -22,6 +22,7 @@ import ctypes
 import functools
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -342,36 +343,40 @@ def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitW
 
 
 _PIPE: dict = {}
+_PIPE_CHUNK = int(os.environ.get("HB_PIPE_CHUNK", str(1 << 21)))  # elements per pinned-pipeline chunk
 
 
-def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=1 << 21, nstreams=3):
-    """Pinned host shares in/out: the layer goes through in chunks on `nstreams` streams so the
-    H2D copy of chunk c+1, the fused kernel on chunk c and the D2H copy of chunk c-1 overlap
-    (PCIe is full duplex; small chunks keep the pipeline fill / drain short).  Same kernel, same
-    triples, same shares as the one-shot path."""
+def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=None):
+    """Pinned host shares in/out, pipelined over three dedicated streams -- host-to-device copies,
+    the fused kernel, device-to-host copies -- joined per chunk by events, so each copy engine is
+    fed back to back (PCIe is full duplex) and no copy waits behind one of the other direction.
+    Same kernel, same triples, same shares as the one-shot path."""
     dev = _dev.device()
+    chunk = chunk or _PIPE_CHUNK
     if dev.index not in _PIPE:
-        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(nstreams))
-    streams = _PIPE[dev.index]
+        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(3))
+    s_in, s_k, s_out = _PIPE[dev.index]
     h0, h1 = x0.data.reshape(-1), x1.data.reshape(-1)
     d0, d1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
     e0, e1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
     o0, o1 = torch.empty(n, dtype=torch.int64, pin_memory=True), torch.empty(n, dtype=torch.int64, pin_memory=True)
     cur = torch.cuda.current_stream()
+    for st in (s_in, s_k, s_out):
+        st.wait_stream(cur)
     lib = _lib.load()
     tv = (views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi())  # same for every chunk
     fn = lib.hb_relu_pair_range
-    for c, lo in enumerate(range(0, n, chunk)):
+    for lo in range(0, n, chunk):
         hi = min(n, lo + chunk)
-        st = streams[c % len(streams)]
-        st.wait_stream(cur)
-        with torch.cuda.stream(st):
+        with torch.cuda.stream(s_in):
             d0[lo:hi].copy_(h0[lo:hi], non_blocking=True)
             d1[lo:hi].copy_(h1[lo:hi], non_blocking=True)
-            _lib.check(fn(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(), e0.data_ptr(),
-                          e1.data_ptr(), *tv, int(drelu_only), st.cuda_stream))
+        s_k.wait_stream(s_in)
+        _lib.check(fn(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(), e0.data_ptr(),
+                      e1.data_ptr(), *tv, int(drelu_only), s_k.cuda_stream))
+        s_out.wait_stream(s_k)
+        with torch.cuda.stream(s_out):
             o0[lo:hi].copy_(e0[lo:hi], non_blocking=True)
             o1[lo:hi].copy_(e1[lo:hi], non_blocking=True)
-    for st in streams:
-        st.synchronize()
+    s_out.synchronize()
     return (ArithShareTensor(0, N, o0.reshape(x0.shape)), ArithShareTensor(1, N, o1.reshape(x1.shape)))
