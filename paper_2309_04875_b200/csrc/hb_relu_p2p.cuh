@@ -6,8 +6,8 @@
 //   1. computes its masked opening (same Kit<W> round math as k_relu_pair / k_stage),
 //   2. stores it straight into the PEER's receive buffer (remote HBM, over NVLink),
 //   3. __syncthreads; one thread fences at system scope and releases the peer's flag[t] = seq(r),
-//   4. waits (acquire) until its own flag[t] >= seq(r) -- the peer's opening of round r is in its
-//      local receive buffer -- and combines.
+//   4. polls its own flag[t] (relaxed) until >= seq(r), then one acquire load of it -- the peer's
+//      opening of round r is in its local receive buffer -- and combines.
 // The transfer of tile t overlaps the math of the other resident tiles: no per-round launches, no
 // host round trips, no NCCL.  Flags are monotonic (seq = epoch * rounds + r + 1) so nothing is
 // reset between launches; each round owns a region of the receive buffer, and a party can only be
@@ -158,7 +158,7 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
             }
           }
         }
-        fence_acq_rel_sys();  // acquire: the peer's stores are visible before the barrier releases the CTA
+        (void)ld_acquire_sys(A.my_flag + tile);  // acquire: the peer's stores are visible before the barrier
       }
       __syncthreads();
       return abort_s == 0;
