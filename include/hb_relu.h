@@ -93,6 +93,7 @@ size_t hb_relu_workspace_bytes(int k, int m, int64_t n);
  * transport.py:129-133) for two parties on two GPUs of one node: the party kernel stores each
  * round's masked opening of a tile straight into the peer's receive buffer and releases a per-tile
  * flag; the peer's kernel acquires it.  Same outputs / triple consumption as hb_relu_round.
+ * Z/2^64 shares (ring_bits = 64) only.
  * hb_relu_p2p_bytes: receive-buffer bytes (identical layout on both sides) and the flag count
  * (uint64 each, zero-initialised once).  seq0 = launches so far x hb_relu_rounds(k, m, drelu_only)
  * (flags are monotonic).  max_ctas: 0 = 3/4 of the co-resident CTAs, > 0 = at most

@@ -439,8 +439,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_tempty[0]);
         }
-        continue;
-      }
+      } else {
       uint32_t hreg[NCH][8];  // PASSES == 2: high part H of each column (mod 2^32)
 #pragma unroll
       for (int p = 0; p < PASSES; ++p, ++u) {
@@ -508,6 +507,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
           if (lane == 0) mbar_arrive(&bar_tempty[buf]);
         }
       }
+      }  // PASSES == 2
     }
     if ((A.dbg & 4) && A.stamps && warp == 0 && lane == 0) {
       A.stamps[blockIdx.x * 8 + 6] = e_read;

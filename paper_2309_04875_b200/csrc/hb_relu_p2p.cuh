@@ -335,8 +335,9 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, cudaStream_t s
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = A.N == 64 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, true>, P2P_TP, 0)
-                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, false>, P2P_TP, 0);
+  // Z/2^64 only (the configs' ring; masks fold away): other rings take the staged path
+  if (A.N != 64) return cudaErrorNotSupported;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, true>, P2P_TP, 0);
   if (e != cudaSuccess) return e;
   // persistent grid with residency margin: 3/4 of the co-resident CTAs for one party on its own GPU,
   // 3/8 per party when both share the device (a deadlock needs BOTH parties partially resident)
@@ -348,17 +349,10 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, cudaStream_t s
   if (getenv("HB_P2P_DEBUG"))
     fprintf(stderr, "[hb_relu_p2p] W=%d %s occ=%d/SM sms=%d grid=%lld per party, tiles=%llu\n", W,
             B ? "both parties" : "one party", occ, sms, grid, (unsigned long long)ntiles);
-  if (B) {
-    if (A.N == 64)
-      k_relu_p2p_dual<W, true><<<(unsigned)(2 * grid), P2P_TP, 0, s>>>(A, A1);
-    else
-      k_relu_p2p_dual<W, false><<<(unsigned)(2 * grid), P2P_TP, 0, s>>>(A, A1);
-  } else {
-    if (A.N == 64)
-      k_relu_p2p<W, true><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
-    else
-      k_relu_p2p<W, false><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
-  }
+  if (B)
+    k_relu_p2p_dual<W, true><<<(unsigned)(2 * grid), P2P_TP, 0, s>>>(A, A1);
+  else
+    k_relu_p2p<W, true><<<(unsigned)grid, P2P_TP, 0, s>>>(A);
   return cudaGetLastError();
 }
 

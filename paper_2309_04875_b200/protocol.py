@@ -200,14 +200,14 @@ def _relu_staged(session: ProtocolSession, x: ArithShareTensor, window: BitWindo
 
 def drelu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> ArithShareTensor:
     """Shared indicator of x >= 0 on the window [m, k) (protocol.py:179-192)."""
-    if session.endpoint.p2p is not None:
+    if session.endpoint.p2p is not None and x.width == 64:
         return relu_p2p(session, x, window, session.endpoint.p2p, drelu_only=True)
     return _relu_staged(session, x, window, drelu_only=True)
 
 
 def relu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> ArithShareTensor:
     """x * DReLU(x[k:m]), the multiply metered as Mult (protocol.py:195-199)."""
-    if session.endpoint.p2p is not None:
+    if session.endpoint.p2p is not None and x.width == 64:
         return relu_p2p(session, x, window, session.endpoint.p2p, drelu_only=False)
     return _relu_staged(session, x, window, drelu_only=False)
 
@@ -223,6 +223,8 @@ def relu_p2p_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: 
         raise ConfigError("relu_p2p_pair expects (party 0, party 1) sessions and shares")
     if x0.width != x1.width or x0.shape != x1.shape:
         raise ConfigError("relu_p2p_pair shares must agree in width and shape")
+    if x0.width != 64:
+        raise ConfigError("the NVLink party kernel runs on Z/2^64 shares (other rings: the staged path)")
     window.check_fits(x0.width)
     N, k, m, w = x0.width, window.k, window.m, window.width
     a0, a1 = _flat(x0.data), _flat(x1.data)
@@ -262,6 +264,8 @@ def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, l
     trace as relu() over any endpoint; both parties must call it for the same layers in order.
     `out` (int64, n elements) avoids an allocation between two parties' launches on one device."""
     window.check_fits(x.width)
+    if x.width != 64:
+        raise ConfigError("the NVLink party kernel runs on Z/2^64 shares (other rings: the staged path)")
     N, k, m, w = x.width, window.k, window.m, window.width
     xd = _flat(x.data)
     n = xd.numel()
