@@ -19,8 +19,8 @@
 // payload sizes (relu_trace); the wire carries the same bytes for w in {8, 16, 32, 64}.
 //
 // Deadlock freedom: the grid is persistent and co-resident with margin (3/4 of the occupancy; both
-// parties in one grid at 3/8 each when they share a device, k_relu_p2p_dual), so CTA c of either
-// party always reaches tile t.  A bounded spin (globaltimer, ~timeout_ms) turns a missing peer into an
+// parties in one grid at 1/2 each when they share a device, k_relu_p2p_dual, party 0 dispatched
+// first), so CTA c of either party always reaches tile t.  A bounded spin (globaltimer, ~timeout_ms) turns a missing peer into an
 // error flag instead of a hang.
 #pragma once
 #include <cstdio>
@@ -339,10 +339,11 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, cudaStream_t s
   if (A.N != 64) return cudaErrorNotSupported;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relu_p2p<W, true>, P2P_TP, 0);
   if (e != cudaSuccess) return e;
-  // persistent grid with residency margin: 3/4 of the co-resident CTAs for one party on its own GPU,
-  // 3/8 per party when both share the device (a deadlock needs BOTH parties partially resident)
+  // persistent grid: 3/4 of the co-resident CTAs for one party on its own GPU (residency margin: a
+  // deadlock needs BOTH parties partially resident); half each for the single-grid two-party harness,
+  // whose party-0 CTAs are dispatched first and so are always all resident
   const long long full = (long long)occ * sms;
-  long long grid = B ? (3 * full) / 8 : (3 * full) / 4;
+  long long grid = B ? full / 2 : (3 * full) / 4;
   if (grid < 1) grid = 1;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if ((u64)grid > ntiles) grid = (long long)ntiles;
