@@ -66,6 +66,8 @@ def parse():
                    help="HBM budget for one ResNet micro-batch's triples (both parties)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                    help="N>1 exchange backend (gloo lets 2 ranks share one GPU for testing)")
+    p.add_argument("--spawn-selftest", action="store_true",
+                   help="CPU check of the --gpus N self-launch: ranks join a gloo group, rank 0 reports")
     return p.parse_args()
 
 
@@ -344,6 +346,23 @@ def run_single(args):
 
 
 # ------------------------------------------------------------------ ResNet private inference (N = 1)
+def micro_batch(model, cfg, batch, parties, budget_gb):
+    """Largest power-of-two split of `batch` whose (a, b, c) triple streams for `parties` parties fit
+    `budget_gb` of HBM (the batch's triples are read once per forward; they are not reusable)."""
+    from paper_2309_04875_b200 import nn
+
+    def triple_bytes(b):
+        return sum(3 * parties * (-(-c * w // 64) * 8 if kind == "bool" else 8 * c)
+                   for (kind, w), c in nn.triple_requirements(model, cfg, b).items())
+
+    mb = batch
+    while mb > 1 and triple_bytes(mb) > budget_gb * 2**30:
+        mb //= 2
+    if batch % mb:
+        raise SystemExit(f"batch {batch} does not split into micro-batches of {mb}")
+    return mb
+
+
 def run_resnet(args):
     """ResNet private inference samples/s, both parties time-sliced on one GPU (BASELINE configs[2,3])."""
     import torch
@@ -362,18 +381,10 @@ def run_resnet(args):
     win = BitWindow(args.k, args.m)
     cfg = models.resnet_relu_config(model, win)
 
-    def triple_bytes(b):  # both parties' (a, b, c) streams for a forward of b samples
-        return sum(3 * 2 * (-(-c * w // 64) * 8 if kind == "bool" else 8 * c)
-                   for (kind, w), c in nn.triple_requirements(model, cfg, b).items())
-
     # micro-batches when the whole batch's triples exceed the HBM budget (ResNet50 b128 at 64x64
     # needs ~208 GB); each micro-batch forward reads its full triple stock from HBM, and the stock
     # is rewound between micro-batches and steps (the dealer is the offline phase, not timed)
-    mb = batch
-    while mb > 1 and triple_bytes(mb) > args.resnet_triple_gb * 2**30:
-        mb //= 2
-    if batch % mb:
-        raise SystemExit(f"batch {batch} does not split into micro-batches of {mb}")
+    mb = micro_batch(model, cfg, batch, 2, args.resnet_triple_gb)
     need = nn.triple_requirements(model, cfg, mb)
     eps = transport.local_pair()
     stores = (dealer.TripleStore(0), dealer.TripleStore(1))
@@ -546,14 +557,18 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
         model, total, shape = models.resnet50(0), args.batch or 512, (3, 64, 64)
     per_pair = max(1, total // max(pairs, 1))
     cfg = models.resnet_relu_config(model, BitWindow(args.k, args.m))
+    # one party per rank: its own triple streams only, micro-batched to the HBM budget (configs[4] at
+    # 2 GPUs is one pair x 4096 samples = ~155 GB of triples per party)
+    mb = micro_batch(model, cfg, per_pair, 1, args.resnet_triple_gb)
     s = torch.cuda.current_stream()
+    used_p2p = False
     if active:
         ep = transport.DistEndpoint(party, rank ^ 1)
         if args.multi_path == "p2p" and ep.enable_p2p() is None:
             log(f"[rank {rank}] NVLink P2P mapping unavailable: staged rounds + {args.backend}")
         used_p2p = ep.p2p is not None
         store = dealer.TripleStore(party)
-        need = nn.triple_requirements(model, cfg, per_pair)
+        need = nn.triple_requirements(model, cfg, mb)
         for i, ((kind, width), count) in enumerate(sorted(need.items())):
             dealer.stock_on_device((store,), (party,), kind, width, count, seed=500 + 31 * pair + i)
         sess = ProtocolSession(ep, store, model.fixed_point)
@@ -562,13 +577,17 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
         x_f = torch.rand((per_pair,) + shape, generator=g, device=dev, dtype=torch.float64)
         enc = torch.floor(x_f * 65536.0 + 0.5).to(torch.int64)
         r = torch.empty_like(enc).random_(generator=g)
-        mine = ArithShareTensor(party, 64, enc + r if party == 0 else -r)
+        share = enc + r if party == 0 else -r
+        mines = [ArithShareTensor(party, 64, share[i:i + mb]) for i in range(0, per_pair, mb)]
         del x_f, enc, r
 
     def fwd():
-        for (kind, width) in need:
-            store.rewind(kind, width)
-        return nn.model_forward(sess, mine, model, cfg)
+        out = None
+        for mine in mines:
+            for (kind, width) in need:
+                store.rewind(kind, width)
+            out = nn.model_forward(sess, mine, model, cfg)
+        return out
 
     if active:
         for _ in range(args.warmup):
@@ -597,7 +616,7 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": f"{args.workload} private inference, batch {pairs * per_pair} over {pairs} pairs",
-                       "batch": pairs * per_pair, "batch_per_pair": per_pair, "pairs": pairs,
+                       "batch": pairs * per_pair, "batch_per_pair": per_pair, "pairs": pairs, "micro_batch": mb,
                        "path": "nn.model_forward per party, ReLU " + (
                            "one-launch NVLink party kernel (openings into the peer's buffer)" if used_p2p
                            else f"staged + {args.backend} send/recv per round"),
@@ -703,9 +722,53 @@ def run_sweep(args):
         json.dump(rows, fh, indent=1)
 
 
+def spawn_cmd(argv, nproc, port):
+    """The driver's own multi-GPU launch line: one rank per GPU, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def self_launch(args, argv):
+    """`bench.py --gpus N` run without torchrun: re-launch as N ranks (one party per GPU; ranks 2i / 2i+1
+    are the parties of pair i) and pass rank 0's JSON line through.  NCCL_DEBUG=INFO (INIT subsystem)
+    puts the communicator lines -- one per rank and device -- on stderr."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    if args.backend == "nccl":
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = spawn_cmd(argv, args.gpus, port)
+    log(f"[bench] self-launch: {' '.join(cmd)}")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def spawn_selftest(args):
+    """--spawn-selftest: the self-launch plumbing on CPU (gloo): every rank joins, rank 0 reports."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t = torch.tensor([rank + 1])
+    dist.all_reduce(t)
+    out = {"selftest": "spawn", "n_gpus": world, "rank_sum": int(t.item()), "pairs": world // 2,
+           "party_of_rank": [r % 2 for r in range(world)], "pair_of_rank": [r // 2 for r in range(world)]}
+    dist.destroy_process_group()
+    return out if rank == 0 else None
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if (args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference" and not args.sweep):
+        sys.exit(self_launch(args, sys.argv[1:]))
+    if args.spawn_selftest:
+        out = spawn_selftest(args)
+    elif args.impl == "reference":
         out = run_reference(args)
     elif args.sweep:
         run_sweep(args)

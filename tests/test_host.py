@@ -253,3 +253,26 @@ def test_dist_relu_rounds_gloo_world2(golden):
     g = golden[0]["base1001_22_16"]
     assert res[0][0] == g["y0_sha"] and res[1][0] == g["y1_sha"]
     assert res[0][1] == g["trace0"] and res[1][1] == g["trace1"]
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus N` without torchrun re-launches itself as N ranks (the driver's SCALE run form);
+    rank 0's JSON line reports n_gpus = N and the pair/party map of ranks 2i / 2i+1."""
+    import json
+    import subprocess
+    import sys
+
+    import bench
+
+    cmd = bench.spawn_cmd(["--gpus", "4"], 4, 29999)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--backend", "gloo",
+                          "--spawn-selftest"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["rank_sum"] == 3 and rec["party_of_rank"] == [0, 1]
