@@ -91,25 +91,34 @@ size_t hb_relu_workspace_bytes(int k, int m, int64_t n);
 /* ---- one party per GPU, openings through the peer's memory (NVLink P2P), one launch per ReLU.
  * Replaces the per-round Endpoint.exchange loop of protocol.relu / drelu (protocol.py:179-199,
  * transport.py:129-133) for two parties on two GPUs of one node: the party kernel stores each
- * round's masked opening of a tile straight into the peer's receive buffer and releases a per-tile
- * flag; the peer's kernel acquires it.  Same outputs / triple consumption as hb_relu_round.
+ * round's masked opening of a tile straight into the peer's receive buffer -- the reference payload
+ * bytes exactly, w-bit packed (transport.py:33-49) -- and releases a per-tile flag at system scope;
+ * the peer's kernel acquires it.  Same outputs / triple consumption as hb_relu_round.
  * Z/2^64 shares (ring_bits = 64) only.
- * hb_relu_p2p_bytes: receive-buffer bytes (identical layout on both sides) and the flag count
- * (uint64 each, zero-initialised once).  seq0 = launches so far x hb_relu_rounds(k, m, drelu_only)
- * (flags are monotonic).  max_ctas: 0 = 3/4 of the co-resident CTAs, > 0 = at most
- * that many.  A peer that does not answer within timeout_s sets *err_dev = 1 (no hang). */
+ * hb_relu_p2p_bytes: receive-buffer bytes of ONE launch (identical layout on both sides) and the
+ * flag count (uint64 each, zero-initialised once).  Consecutive launches must alternate between two
+ * such regions (transport.PeerLink: launch parity), since a peer may start launch k+1 while this
+ * party still reads launch k's last round.  seq0 = rounds of all earlier launches on these flags
+ * (hb_relu_rounds each; flags are monotonic).  The launch is cooperative: max_ctas 0 = every
+ * co-resident CTA, > 0 = at most that many.  A peer that does not answer within timeout_s sets
+ * *err_dev = 1 (no hang).  wire_bytes_dev (optional, one uint64 accumulated by the kernel) counts
+ * the bytes stored into the peer's buffer = hb_relu_p2p_wire_bytes. */
 uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* ntiles);
+uint64_t hb_relu_p2p_wire_bytes(int k, int m, int64_t n, int drelu_only);
 int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
                 hb_triples_t bool_w, hb_triples_t arith_n, void* recv, const uint64_t* my_flags, void* peer_recv,
                 uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
-                void* stream);
-/* Both parties' party kernels in ONE launch on one device (CTAs split between the parties), the
- * openings going through each other's receive buffers exactly as across two GPUs: the single-GPU
- * harness of hb_relu_p2p (recv1 / flags1 play the peer's mapped buffers for party 0 and vice versa). */
+                uint64_t* wire_bytes_dev, void* stream);
+/* Both parties' party kernels in ONE launch on one device (max_ctas0 / max_ctas1 CTAs per party, 0 =
+ * half the co-resident CTAs each), the openings going through each other's receive buffers exactly
+ * as across two GPUs: the single-GPU harness of hb_relu_p2p (recv1 / flags1 play the peer's mapped
+ * buffers for party 0 and vice versa).  sys_scope = 0: gpu-scope flags (the scope both parties
+ * share on one device); 1: the system-scope protocol of hb_relu_p2p, for measurement. */
 int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
                      uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
-                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas,
-                     double timeout_s, int* err_dev, int drelu_only, void* stream);
+                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas0,
+                     int max_ctas1, int sys_scope, double timeout_s, int* err_dev, int drelu_only,
+                     uint64_t* wire_bytes_dev, void* stream);
 /* CUDA IPC for the receive buffers / flags of a party on another GPU (64-byte handles); the buffers
  * are whole allocations (hb_dev_alloc, zero-filled) so a handle maps exactly them. */
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr);

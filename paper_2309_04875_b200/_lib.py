@@ -63,13 +63,15 @@ _SIGS = {
     "hb_relu_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "hb_relu_p2p_bytes": (ctypes.c_uint64, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_int64)]),
+    "hb_relu_p2p_wire_bytes": (ctypes.c_uint64, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
     "hb_relu_p2p": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p,
                                    Triples, Triples, ctypes.c_void_p, u64p, ctypes.c_void_p, u64p, ctypes.c_uint64,
-                                   ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+                                   ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int, u64p,
+                                   ctypes.c_void_p]),
     "hb_relu_p2p_pair": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p, u64p,
                                         u64p, Triples, Triples, Triples, Triples, ctypes.c_void_p, ctypes.c_void_p,
-                                        u64p, u64p, ctypes.c_uint64, ctypes.c_int, ctypes.c_double,
-                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+                                        u64p, u64p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_void_p, ctypes.c_int, u64p, ctypes.c_void_p]),
     "hb_dev_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "hb_dev_free": (ctypes.c_int, [ctypes.c_void_p]),
     "hb_ipc_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),

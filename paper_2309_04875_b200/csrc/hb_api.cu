@@ -26,7 +26,7 @@ using hb::u64;
   cudaError_t hb_pair_dispatch_##lo##_##hi(int W, const hb::PairArgs& A, cudaStream_t s);          \
   cudaError_t hb_stage_dispatch_##lo##_##hi(int W, const hb::StageArgs& A, int L, cudaStream_t s); \
   cudaError_t hb_p2p_dispatch_##lo##_##hi(int W, const hb::P2PArgs& A, const hb::P2PArgs* B, int max_ctas, \
-                                          cudaStream_t s);                                             \
+                                          int max_ctas1, int dual_sys, cudaStream_t s);                \
   unsigned long long hb_p2p_layout_##lo##_##hi(int W, unsigned long long n, int drelu_only,        \
                                                unsigned long long* ntiles);                        \
   size_t hb_pair_smem_##lo##_##hi(int W);
@@ -257,17 +257,32 @@ uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* nti
   return b;
 }
 
+uint64_t hb_relu_p2p_wire_bytes(int k, int m, int64_t n, int drelu_only) {
+  // what hb_relu_p2p stores into the peer's buffer per launch: every bool round's segments as exact
+  // w-bit streams (ceil(n w / 8) bytes each), 8 bytes per element and segment of the arith rounds
+  const int w = k - m;
+  if (w < 2 || w > 64 || n < 0) return 0;
+  const int L = levels(w), R = L + (drelu_only ? 2 : 3);
+  const uint64_t seg = ((uint64_t)n * (uint64_t)w + 7) / 8;
+  uint64_t b = 0;
+  for (int r = 0; r < R; ++r) b += r == 0 ? 2 * seg : (r <= L ? 4 * seg : 16 * (uint64_t)n);
+  return b;
+}
+
 namespace {
 int p2p_args(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
              const hb_triples_t& boolw, const hb_triples_t& arith, void* recv, const uint64_t* my_flags,
              void* peer_recv, uint64_t* peer_flags, uint64_t seq0, double timeout_s, int* err_dev, int drelu_only,
-             hb::P2PArgs& A) {
+             uint64_t* wire_bytes, hb::P2PArgs& A) {
   int rc = check_window(ring_bits, k, m);
   if (rc) return rc;
+  if (ring_bits != 64) return fail(HB_ERR_CONFIG, "the P2P party kernel runs on Z/2^64 shares (ring_bits %d)", ring_bits);
   if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
   if (n < 0) return fail(HB_ERR_CONFIG, "negative element count");
   if (n > 0 && (!recv || !my_flags || !peer_recv || !peer_flags || !err_dev))
     return fail(HB_ERR_CONFIG, "null p2p buffer");
+  if ((reinterpret_cast<uintptr_t>(recv) | reinterpret_cast<uintptr_t>(peer_recv)) & 255)
+    return fail(HB_ERR_CONFIG, "p2p receive buffers must be 256-byte aligned");
   const int w = k - m, L = levels(w);
   const int64_t nb = n * (1 + 2 * (int64_t)L), na = (drelu_only ? 1 : 2) * n;
   if ((rc = check_triples(boolw, "bool", w, nb, party)) || (rc = check_triples(arith, "arith", ring_bits, na, party)))
@@ -285,6 +300,8 @@ int p2p_args(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* 
   A.peer_flag = reinterpret_cast<unsigned long long*>(peer_flags);
   A.timeout_ns = (u64)(timeout_s * 1e9);
   A.err = err_dev;
+  A.wire_bytes = reinterpret_cast<unsigned long long*>(wire_bytes);
+  A.stamps = nullptr;
   return HB_OK;
 }
 }  // namespace
@@ -292,27 +309,30 @@ int p2p_args(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* 
 int hb_relu_p2p(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
                 hb_triples_t boolw, hb_triples_t arith, void* recv, const uint64_t* my_flags, void* peer_recv,
                 uint64_t* peer_flags, uint64_t seq0, int max_ctas, double timeout_s, int* err_dev, int drelu_only,
-                void* stream) {
+                uint64_t* wire_bytes_dev, void* stream) {
   hb::P2PArgs A;
   const int rc = p2p_args(party, ring_bits, k, m, n, x, y, boolw, arith, recv, my_flags, peer_recv, peer_flags, seq0,
-                          timeout_s, err_dev, drelu_only, A);
+                          timeout_s, err_dev, drelu_only, wire_bytes_dev, A);
   if (rc || n == 0) return rc;
-  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A, (const hb::P2PArgs*)nullptr, max_ctas, S(stream)),
-                     "hb_relu_p2p");
+  return cuda_status(
+      HB_RANGE_CALL(hb_p2p_dispatch, k - m, A, (const hb::P2PArgs*)nullptr, max_ctas, 0, 0, S(stream)),
+      "hb_relu_p2p");
 }
 
 int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
                      uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
-                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas,
-                     double timeout_s, int* err_dev, int drelu_only, void* stream) {
+                     void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas0,
+                     int max_ctas1, int sys_scope, double timeout_s, int* err_dev, int drelu_only,
+                     uint64_t* wire_bytes_dev, void* stream) {
   hb::P2PArgs A0, A1;
   int rc = p2p_args(0, ring_bits, k, m, n, x0, y0, bool0, arith0, recv0, flags0, recv1, flags1, seq0, timeout_s,
-                    err_dev, drelu_only, A0);
+                    err_dev, drelu_only, wire_bytes_dev, A0);
   if (rc) return rc;
   rc = p2p_args(1, ring_bits, k, m, n, x1, y1, bool1, arith1, recv1, flags1, recv0, flags0, seq0, timeout_s, err_dev,
-                drelu_only, A1);
+                drelu_only, wire_bytes_dev, A1);
   if (rc || n == 0) return rc;
-  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A0, &A1, max_ctas, S(stream)), "hb_relu_p2p_pair");
+  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A0, &A1, max_ctas0, max_ctas1, sys_scope, S(stream)),
+                     "hb_relu_p2p_pair");
 }
 
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr) {
@@ -320,6 +340,9 @@ int hb_dev_alloc(uint64_t bytes, void** dev_ptr) {
   // allocator's segment), zero-filled
   cudaError_t e = cudaMalloc(dev_ptr, bytes ? bytes : 1);
   if (e == cudaSuccess) e = cudaMemset(*dev_ptr, 0, bytes ? bytes : 1);
+  // the zero fill must land before the buffer is exported or a kernel on any stream (or the peer's
+  // kernel, through IPC) stores into it: cudaMemset is asynchronous to the host
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return cuda_status(e, "hb_dev_alloc");
 }
 
@@ -440,6 +463,8 @@ int hb_relu(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x
     if (rc) return rc;
     if (r < last) {
       const int64_t bytes = hb_relu_round_bytes(ring_bits, k, m, n, r);
+      // the callback may read `own` / write `peer` with any copy engine or stream: finish the round first
+      if ((rc = cuda_status(cudaStreamSynchronize(S(stream)), "hb_relu"))) return rc;
       if (exchange(user, hb_relu_round_tag(k, m, r), own, peer, bytes, stream) != 0)
         return fail(HB_ERR_TRANSPORT, "exchange failed in round %d", r);
     }

@@ -88,11 +88,11 @@ cudaError_t HB_CAT(hb_stage_dispatch_, HB_W_LO, HB_W_HI)(int W, const hb::StageA
 }
 
 cudaError_t HB_CAT(hb_p2p_dispatch_, HB_W_LO, HB_W_HI)(int W, const hb::P2PArgs& A, const hb::P2PArgs* B, int max_ctas,
-                                                       cudaStream_t s) {
+                                                       int max_ctas1, int dual_sys, cudaStream_t s) {
   switch (W) {
 #define HB_CASE(w) \
   case w:          \
-    if (w >= HB_W_LO && w <= HB_W_HI) return hb::launch_p2p<(w >= HB_W_LO && w <= HB_W_HI) ? w : HB_W_LO>(A, B, max_ctas, s); \
+    if (w >= HB_W_LO && w <= HB_W_HI) return hb::launch_p2p<(w >= HB_W_LO && w <= HB_W_HI) ? w : HB_W_LO>(A, B, max_ctas, max_ctas1, dual_sys, s); \
     break;
 #include "hb_widths.inc"
 #undef HB_CASE

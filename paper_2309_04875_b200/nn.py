@@ -353,21 +353,33 @@ def _limb_planes(x_nchw: torch.Tensor, stream) -> torch.Tensor:
     return planes
 
 
-def _tma_box_ok(oh: int, ow: int) -> bool:
-    """Output geometry tiles into 128-pixel (batch, oh, ow) boxes (hb_tma_conv_box)."""
+def _tma_box(oh: int, ow: int):
+    """The 128-pixel (batch, oh, ow) output box hb_tma_conv_box picks, as (bb, bh, bw), or None when
+    the output geometry does not tile (hb_conv_tma.cu:573-591)."""
     if ow >= 128:
-        return ow % 128 == 0
+        return (1, 1, 128) if ow % 128 == 0 else None
     if 128 % ow:
-        return False
+        return None
     rows = 128 // ow
-    return oh % rows == 0 if oh >= rows else rows % oh == 0
+    if oh >= rows:
+        return (1, rows, ow) if oh % rows == 0 else None
+    return (rows // oh, oh, ow) if rows % oh == 0 else None
+
+
+def _tma_box_ok(oh: int, ow: int, stride: int = 1) -> bool:
+    """Mirror of every geometry check hb_tma_conv makes before encoding its tensor maps: the box
+    tiles the output, and the input window it reads (box extent x conv stride) is at most 256 per
+    dimension (hb_conv_tma.cu:655-657); the traversal stride is at most 8."""
+    box = _tma_box(oh, ow)
+    return box is not None and stride <= 8 and box[2] * stride <= 256 and box[1] * stride <= 256
 
 
 def _tma_ok(x_nchw: torch.Tensor, geom, lw: _LimbWeight) -> bool:
     b, c, h, w = x_nchw.shape
     kh, kw, stride, pad = geom
     oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
-    return RING_GEMM == "tc" and lw.wl_tma is not None and stride <= 8 and b > 0 and _tma_box_ok(oh, ow)
+    return (RING_GEMM == "tc" and lw.wl_tma is not None and c % TMA_KB == 0 and b > 0
+            and _tma_box_ok(oh, ow, stride))
 
 
 def _gemm_tc(x_nchw: torch.Tensor, geom, lw: _LimbWeight, party: int, frac: int,

@@ -213,10 +213,12 @@ def relu(session: ProtocolSession, x: ArithShareTensor, window: BitWindow) -> Ar
 
 
 def relu_p2p_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitWindow, links,
-                  drelu_only: bool = False):
+                  drelu_only: bool = False, sys_scope: bool = False):
     """Both parties' NVLink party kernels in one launch on this GPU (hb_relu_p2p_pair), the openings
     going through each other's receive buffers (`links` = transport.local_p2p_pair()) exactly as
-    relu_p2p does across two GPUs.  Same shares / triples / meter as relu_pair and relu."""
+    relu_p2p does across two GPUs.  Same shares / triples / meter as relu_pair and relu.
+    sys_scope: run the system-scope flag protocol of the cross-GPU kernel (measurement) instead of
+    the gpu scope both parties share on one device."""
     s0, s1 = sessions
     l0, l1 = links
     if (s0.party, s1.party) != (0, 1) or (x0.party, x1.party) != (0, 1):
@@ -246,12 +248,16 @@ def relu_p2p_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: 
     seq0 = l0.seq
     l0.seq += rounds
     l1.seq += rounds
+    r0, _ = l0.region()
+    r1, _ = l1.region()
     y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
     y1 = torch.empty(n, dtype=torch.int64, device=a0.device)
+    wc = l0.wire_counter
     _lib.check(lib.hb_relu_p2p_pair(N, k, m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
                                     views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),
-                                    l0.recv, l1.recv, l0.flags, l1.flags, seq0, l0.max_ctas, l0.timeout_s,
-                                    l0.err.data_ptr(), int(drelu_only), _stream()))
+                                    r0, r1, l0.flags, l1.flags, seq0, l0.max_ctas, l1.max_ctas, int(sys_scope),
+                                    l0.timeout_s, l0.err.data_ptr(), int(drelu_only),
+                                    None if wc is None else wc.data_ptr(), _stream()))
     l0.after_launch(torch.cuda.current_stream())
     return (_wrap(ArithShareTensor, 0, N, y0, x0.data, x0.shape), _wrap(ArithShareTensor, 1, N, y1, x1.data, x1.shape))
 
@@ -282,14 +288,16 @@ def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, l
     rounds = lib.hb_relu_rounds(k, m, int(drelu_only))
     seq0 = link.seq
     link.seq += rounds
+    own, peer = link.region()
     session.endpoint.meter.record_rounds(_relu_trace(n, k, m, N, bool(drelu_only)))
     y = torch.empty(n, dtype=torch.int64, device=xd.device) if out is None else out.reshape(-1)
     if y.numel() != n or y.dtype != torch.int64 or not y.is_cuda:
         raise ConfigError("relu_p2p out must be a CUDA int64 tensor of the input's size")
     st = _stream() if stream is None else stream.cuda_stream
+    wc = link.wire_counter
     _lib.check(lib.hb_relu_p2p(session.party, N, k, m, n, xd.data_ptr(), y.data_ptr(), bv.abi(), av.abi(),
-                               link.recv, link.flags, link.peer_recv, link.peer_flags, seq0,
-                               link.max_ctas, link.timeout_s, link.err.data_ptr(), int(drelu_only), st))
+                               own, link.flags, peer, link.peer_flags, seq0, link.grid, link.timeout_s,
+                               link.err.data_ptr(), int(drelu_only), None if wc is None else wc.data_ptr(), st))
     link.after_launch(torch.cuda.current_stream() if stream is None else stream)
     return _wrap(ArithShareTensor, x.party, N, y, x.data, x.shape)
 

@@ -286,3 +286,16 @@ def sim_model_inputs(mc):
     rng = np.random.default_rng(91 + mc["batch"])
     shape = (mc["batch"], 1, 8, 8) if mc["arch"] == "cnn" else (mc["batch"], 64)
     return rng.uniform(0.0, 1.0, shape), rng.integers(0, 10, mc["batch"])
+
+
+# ---------------------------------------------------------------- window search (search.py:159-334)
+SEARCH_CASES = [
+    dict(name="search_eco_cnn", kind="eco", seed=4, batch=24),
+    dict(name="search_budget_cnn_quarter", kind="budget", budget="1/4", widths=[0, 4, 8, 12, 16], seed=6, batch=24),
+    dict(name="search_budget_cnn_eighth", kind="budget", budget="1/8", widths=[0, 2, 4, 6, 8], seed=8, batch=24),
+]
+
+
+def search_inputs(case):
+    rng = np.random.default_rng(123 + case["batch"] + case["seed"])
+    return rng.uniform(0.0, 1.0, (case["batch"], 1, 8, 8)), rng.integers(0, 10, case["batch"])

@@ -167,3 +167,72 @@ def test_limb_gemm_exact_at_resnet_width():
     for p in (0, 1):
         y = nn.linear_forward(_Sess, ArithShareTensor(p, 64, x), w, b)
         assert np.array_equal(y.data, ON.linear(x, p, w, b))
+
+
+def _conv_geometries(model):
+    """Every distinct conv of a model: (cin, cout, k, stride, pad, H, W, weight name), H x W its input."""
+    seen, out = set(), []
+
+    def walk(layers, shape):
+        for L in layers:
+            if isinstance(L, nn.Residual):
+                walk(L.body, shape)
+                walk(L.shortcut, shape)
+                shape = nn._out_shape(L.body, shape)
+                continue
+            if isinstance(L, nn.Conv2d):
+                key = (L.in_channels, L.out_channels, L.kh, L.stride, L.pad, shape[1], shape[2])
+                if key not in seen:
+                    seen.add(key)
+                    out.append(key + (L.weight, L.bias))
+            shape = nn._layer_shape(L, shape)
+
+    walk(model.layers, model.input_shape)
+    return out
+
+
+def _conv_cases():
+    cases = []
+    for name, model, batch in (("rn18", models.resnet18_cifar(0), 2), ("rn50", models.resnet50(0), 1)):
+        for g in _conv_geometries(model):
+            cases.append(pytest.param(model, batch, g, id=f"{name}-c{g[0]}-o{g[1]}-k{g[2]}-s{g[3]}-{g[5]}x{g[6]}"))
+    return cases
+
+
+@pytest.mark.parametrize("model,batch,geom", _conv_cases())
+def test_every_resnet_conv_bit_exact(model, batch, geom):
+    """Every distinct ResNet18-CIFAR and ResNet50 (64x64) conv through nn.conv2d_forward -- the TMA
+    tcgen05 kernel (one-pass N_T = 64, two-pass N_T = 128 for N >= 128 at K up to 4608), the stem
+    through im2col limb planes, strided 1x1 shortcuts -- equals the reference conv
+    (nn.py:227-243, restated in oracle/hb_oracle_nn.conv2d) share for share, both parties."""
+    cin, cout, k, stride, pad, h, w, wname, bname = geom
+    rng = np.random.default_rng(cin * 1000 + cout + h)
+    x = np.frombuffer(rng.bytes(8 * batch * cin * h * w), dtype="<u8").copy().reshape(batch, cin, h, w)
+    wt, bias = model.weights[wname], model.weights[bname] + np.float32(0.01)
+    layer = nn.Conv2d(cin, cout, k, k, stride, pad, weight="w", bias="b")
+    for p in (0, 1):
+        y = nn.conv2d_forward(_Sess, ArithShareTensor(p, 64, x), layer, wt, bias)
+        want = ON.conv2d(x, p, cin, cout, k, k, stride, pad, wt, bias)
+        assert np.array_equal(np.asarray(y.data), want), (geom, p)
+
+
+def _deep_block_model(cin, cout, side):
+    """One ResNet18 down-sampling basic block (3x3 stride-2 conv, 3x3 conv, strided 1x1 shortcut, the
+    residual add fused into the second conv's epilogue) at layer3 / layer4 geometry."""
+    ini = models._Init(6)
+    layers = models._basic_block(ini, "blk", cin, cout, 2, 0)
+    layers += [nn.AvgPool(side // 2, side // 2, side // 2), nn.Flatten(), ini.linear("fc", cout, 10)]
+    return nn.ModelSpec(FixedPointConfig(), (cin, side, side), layers, ini.weights)
+
+
+@pytest.mark.parametrize("cin,cout,side", [(128, 256, 16), (256, 512, 8)], ids=["layer3", "layer4"])
+def test_fused_residual_block_at_layer3_layer4_geometry(cin, cout, side):
+    """The two-pass k_conv_tma<128, 2, J> with the fused residual epilogue at ResNet18 layer3 / layer4
+    shapes (K = 1152 / 2304 / 4608): logits equal the oracle's run_local_forward exactly."""
+    model = _deep_block_model(cin, cout, side)
+    x_f = np.random.default_rng(cin).uniform(0, 1, (2, cin, side, side))
+    cfg = nn.ReluConfig([BitWindow(22, 14)])
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    want, _, _ = ON.run_local_forward(layers, model.input_shape, model.weights, [(22, 14)], x_f, 5)
+    logits, _, _, _ = nn.run_local_forward(model, cfg, x_f, 5, pair=True, layer_logs=False)
+    assert np.array_equal(logits, want)

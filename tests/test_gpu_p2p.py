@@ -87,6 +87,107 @@ def test_p2p_sequence_growth_and_large():
         assert torch.equal(r0.data, q0.data) and torch.equal(r1.data, q1.data)
 
 
+def test_p2p_parties_with_different_grids():
+    """The parties' grids need not match (tile = cta, cta + grid, ...): party 0 with 37 CTAs and party
+    1 with 101 complete bit-exact (no cross-wait, no timeout); and the agreed grid of a PeerLink pair is
+    the smaller request."""
+    n, k, m = (1 << 18) + 5, 22, 14
+    x0, x1 = gc.baseline_inputs(n, seed=21)
+    curs = O.stocked_cursors(n, k - m, 64, seed=21)
+    y0o, y1o, _, _ = O.relu_pair(x0, x1, 64, k, m, curs)
+    s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=21)
+    t0 = ArithShareTensor(0, 64, torch.from_numpy(x0.view(np.int64)).cuda())
+    t1 = ArithShareTensor(1, 64, torch.from_numpy(x1.view(np.int64)).cuda())
+    r0, r1 = _p2p_pair(s0, s1, t0, t1, BitWindow(k, m), transport.local_p2p_pair((37, 101)))
+    assert np.array_equal(r0.data.cpu().numpy().view(np.uint64), y0o)
+    assert np.array_equal(r1.data.cpu().numpy().view(np.uint64), y1o)
+
+
+@pytest.mark.parametrize("sys_scope", [False, True], ids=["gpu_scope", "sys_scope"])
+def test_p2p_scopes_agree(sys_scope):
+    """The same-device harness (gpu-scope flags) and the cross-GPU protocol (system scope) give the
+    same shares."""
+    n, k, m = 50000, 22, 16
+    x0, x1 = gc.baseline_inputs(n, seed=31)
+    curs = O.stocked_cursors(n, k - m, 64, seed=31)
+    y0o, y1o, _, _ = O.relu_pair(x0, x1, 64, k, m, curs)
+    s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=31)
+    links = transport.local_p2p_pair()
+    links[0].timeout_s = 20.0
+    r0, r1 = protocol.relu_p2p_pair((s0, s1), ArithShareTensor(0, 64, x0), ArithShareTensor(1, 64, x1),
+                                    BitWindow(k, m), links, sys_scope=sys_scope)
+    links[0].check(sync=True)
+    assert np.array_equal(r0.data, y0o) and np.array_equal(r1.data, y1o)
+
+
+@pytest.mark.parametrize("k,m", [(22, 17), (22, 16), (22, 0), (22, 14), (64, 0), (40, 7)],
+                         ids=["w5", "w6", "w22", "w8", "w64", "w33"])
+def test_p2p_wire_bytes_are_the_reference_payload(k, m):
+    """What crosses NVLink = the reference payload (transport.py:33-49, protocol.py:62-72): the kernel
+    counts every byte it stores into the peer's buffer; per launch that equals hb_relu_p2p_wire_bytes,
+    which is the reference trace less only the zero padding of each round's last 64-bit word."""
+    from paper_2309_04875_b200 import _lib
+
+    lib = _lib.load()
+    for n in (3000, (1 << 16) + 37):
+        w = k - m
+        x0, x1 = gc.baseline_inputs(n, seed=w)
+        s0, s1, _ = stocked_sessions_for_relu(n, w, 64, seed=w)
+        links = transport.local_p2p_pair()
+        counter = links[0].count_wire()
+        _p2p_pair(s0, s1, ArithShareTensor(0, 64, x0), ArithShareTensor(1, 64, x1), BitWindow(k, m), links)
+        ours = int(lib.hb_relu_p2p_wire_bytes(k, m, n, 0))
+        assert int(counter.item()) == 2 * ours  # both parties of the one-launch harness count into it
+        trace = protocol.relu_trace(n, BitWindow(k, m), 64)
+        ref = sum(b for _, b in trace)
+        assert 0 <= ref - ours < 8 * len(trace), (ref, ours)
+        if (n * w) % 64 == 0:
+            assert ours == ref
+
+
+def test_p2p_parties_on_two_streams_layer_sequence():
+    """Each party's kernel is its own launch on its own stream (as on two GPUs), so a party can start
+    the next layer while its peer still reads the previous layer's last round.  Layers whose receive
+    layouts overlap (a narrow large layer, then a wide larger one; a small layer, then a large one)
+    stay bit-exact: consecutive launches alternate between the two receive regions."""
+    links = transport.local_p2p_pair(max_ctas=64)
+    links[0].timeout_s = links[1].timeout_s = 30.0
+    st = [torch.cuda.Stream(), torch.cuda.Stream()]
+    layers = [((1 << 20), (22, 20)), ((1 << 21), (64, 0)), (25088, (22, 14)), (802816, (22, 14)),
+              ((1 << 20) + 3, (22, 20)), ((1 << 21), (64, 0))]
+    sess = [stocked_sessions_for_relu(n, k - m, 64, seed=40 + i)[:2] for i, (n, (k, m)) in enumerate(layers)]
+    ins = [gc.baseline_inputs(n, seed=50 + i) for i, (n, _) in enumerate(layers)]
+    dev_in = [(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda()) for a, b in ins]
+    # grow the buffers to the largest layer first (a growth synchronises the device)
+    sizes = [_lib_bytes(n, km) for n, km in layers]
+    links[0].ensure(max(b for b, _ in sizes), max(t for _, t in sizes))
+    torch.cuda.synchronize()
+    outs = []
+    for i, (n, (k, m)) in enumerate(layers):
+        ys = []
+        for p in (0, 1):
+            with torch.cuda.stream(st[p]):
+                ys.append(protocol.relu_p2p(sess[i][p], ArithShareTensor(p, 64, dev_in[i][p]), BitWindow(k, m),
+                                            links[p], stream=st[p]))
+        outs.append(ys)
+    for lk in links:
+        lk.check(sync=True)
+    for i, (n, (k, m)) in enumerate(layers):
+        q0, q1 = stocked_sessions_for_relu(n, k - m, 64, seed=40 + i)[:2]
+        w0, w1 = protocol.relu_pair((q0, q1), ArithShareTensor(0, 64, dev_in[i][0]), ArithShareTensor(1, 64, dev_in[i][1]),
+                                    BitWindow(k, m))
+        assert torch.equal(outs[i][0].data, w0.data) and torch.equal(outs[i][1].data, w1.data), i
+
+
+def _lib_bytes(n, km):
+    import ctypes
+
+    from paper_2309_04875_b200 import _lib
+
+    nt = ctypes.c_int64(0)
+    return _lib.load().hb_relu_p2p_bytes(km[0], km[1], n, 0, ctypes.byref(nt)), nt.value
+
+
 def test_p2p_missing_peer_times_out():
     """Only party 0 runs (relu_p2p, one party): its kernel gives up after the timeout and the
     link raises instead of hanging."""

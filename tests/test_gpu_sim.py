@@ -70,3 +70,25 @@ def test_sim_forward_resnet18_runs():
     ranges = simulator.collect_activation_ranges(model, x_f)
     assert set(ranges) == set(range(model.n_groups)) and all(2 <= v <= 64 for v in ranges.values())
     _ = torch
+
+
+@pytest.mark.parametrize("case", gc.SEARCH_CASES, ids=[c["name"] for c in gc.SEARCH_CASES])
+def test_window_search_vs_reference(golden, case):
+    """search_eco / search_budget over the GPU simulator return the reference's windows, accuracy,
+    baseline, bit fraction and search trace (tests/golden/golden_search.json, made by running the
+    reference search on its desk CNN)."""
+    import json
+    import os
+
+    from paper_2309_04875_b200 import search
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_search.json")) as fh:
+        want = json.load(fh)[case["name"]]
+    model = _desk("cnn", golden[1])
+    x_f, labels = gc.search_inputs(case)
+    if case["kind"] == "eco":
+        res = search.search_eco(model, x_f, labels, seed=case["seed"])
+    else:
+        res = search.search_budget(model, x_f, labels, case["budget"], threshold=case.get("threshold"),
+                                   candidate_widths=tuple(case["widths"]), seed=case["seed"])
+    assert res.to_json() == want
