@@ -204,6 +204,58 @@ def cpu_baseline(k, m, ring_bits, steps=2, warmup=1):
                       f"pair (oracle/hb_oracle.py incl. unpackbits codec, 2 party threads) per worker process"}
 
 
+def model_baselines(cpu_relu_rate, batch=64):
+    """SURVEY 8(d) model-level context on this host (untimed by the bench clock, N = 1 only):
+    * desk_cnn: the reference's desk CNN (models.py:50-72; weights = the reference's own draws, the
+      same generator) through run_local_forward (cli.py:159-180) -- the reference algorithm on the host
+      (oracle port, 2 party threads) vs this package on the GPU (pair mode, numpy in / logits out),
+      same inputs, seed and windows; the logits must be identical.
+    * resnet18_cpu_estimate: seconds per sample for ONE party pair on the host, an ESTIMATE (the
+      reference cannot express residual blocks): ReLU elements / the measured host ReLU rate (all
+      cores) + 2 x conv MACs / the measured host ring-conv MAC rate (oracle conv2d, uint64 matmul,
+      on a layer1-shaped conv of one image)."""
+    import numpy as np
+
+    from oracle import hb_oracle_nn as ON
+    from paper_2309_04875_b200 import models, nn
+    from paper_2309_04875_b200.ring import BitWindow
+
+    model = models.desk_cnn(11)
+    wins = [BitWindow(20, 8), BitWindow(19, 6)]
+    cfg = nn.ReluConfig(wins)
+    x_f = np.random.default_rng(2024).uniform(0.0, 1.0, (batch, 1, 8, 8))
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    t0 = time.perf_counter()
+    ref_logits, _, _ = ON.run_local_forward(layers, model.input_shape, model.weights, [(w.k, w.m) for w in wins],
+                                            x_f, 5)
+    t_cpu = time.perf_counter() - t0  # includes the host dealer (the reference's run_local_forward excludes it)
+    nn.run_local_forward(model, cfg, x_f, 5, pair=True)  # warm-up (kernel loads, weight encoding)
+    logits, _, _, gpu_ms = nn.run_local_forward(model, cfg, x_f, 5, pair=True)
+    desk = {"batch": batch, "windows": [[w.k, w.m] for w in wins], "seed": 5,
+            "cpu_samples_per_s": batch / t_cpu, "cpu_cores": 2, "cpu_kind": "port",
+            "cpu_note": "oracle/hb_oracle_nn.run_local_forward (reference algorithm, 2 party threads); wall "
+                        "includes the host dealer",
+            "gpu_samples_per_s": batch / (gpu_ms / 1e3),
+            "gpu_note": "nn.run_local_forward(pair=True) wall_ms (host shares in, logits out; dealer excluded, "
+                        "as cli.py:170-177 times it)",
+            "logits_identical": bool(np.array_equal(logits, ref_logits))}
+    # ring-conv MAC rate of the reference algorithm on this host (one party, one image, layer1 shape)
+    rng = np.random.default_rng(3)
+    xs = rng.integers(0, 2**63, (1, 64, 32, 32), dtype=np.uint64)
+    wt = rng.normal(0, 0.05, (64, 64, 3, 3)).astype(np.float32)
+    t0 = time.perf_counter()
+    ON.conv2d(xs, 0, 64, 64, 3, 3, 1, 1, wt, np.zeros(64, np.float32))
+    conv_rate = 64 * 64 * 9 * 32 * 32 / (time.perf_counter() - t0)
+    rn = models.resnet18_cifar(0)
+    relu_per_sample = sum(c for _, c in rn.relu_sites())
+    macs = models.conv_macs(rn)
+    est = relu_per_sample / cpu_relu_rate + 2 * macs / conv_rate
+    return desk, {"seconds_per_sample_per_pair": est, "label": "ESTIMATE (not a run)",
+                  "relu_elems_per_sample": relu_per_sample, "host_relu_elems_per_s": cpu_relu_rate,
+                  "conv_macs_per_sample": macs, "host_conv_macs_per_s_per_party": conv_rate,
+                  "samples_per_s": 1.0 / est}
+
+
 # ------------------------------------------------------------------ N = 1: fused pair
 def run_single(args):
     import torch
@@ -324,6 +376,9 @@ def run_single(args):
                "path": "protocol.relu_pair with pinned host shares in and host shares out", "steps": reps}
 
     cpu = None if args.no_cpu_baseline else cpu_baseline(k, m, N)
+    desk = rn_est = None
+    if cpu is not None and args.path == "pair":
+        desk, rn_est = model_baselines(cpu["value"])
     resnet = None
     if not args.no_resnet and args.path == "pair" and args.logn == 24:
         del stores, sessions, x0, x1, y0, y1
@@ -334,7 +389,8 @@ def run_single(args):
         ra.workload, ra.batch, ra.steps, ra.warmup = "resnet18", 512, 3, 2
         r = run_resnet(ra)
         resnet = {"metric": r["metric"], "value": r["value"], "unit": r["unit"], "ms_per_step": r["ms_per_step"],
-                  "config": r["config"], "steps": r["steps"], "warmup": r["warmup"]}
+                  "config": r["config"], "steps": r["steps"], "warmup": r["warmup"],
+                  "logits_check": r["logits_check"], "cpu_estimate": rn_est}
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -355,7 +411,7 @@ def run_single(args):
                      "frac_vs_survey_H": (2 * n * bpe["survey_H"] / (launch_ms / 1e3) / 1e9) / peak,
                      "kernel": "hb::" + kernel, "traffic_source": traffic_src, "launch_ms": launch_ms},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
-        "resnet18": resnet,
+        "resnet18": resnet, "desk_cnn": desk,
     }
 
 

@@ -81,6 +81,7 @@ int fail(int code, const char* fmt, ...) {
 
 int cuda_status(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return HB_OK;
+  (void)cudaGetLastError();  // a failed launch must not surface again in the next call's status
   return fail(HB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 

@@ -621,7 +621,10 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, int max_ctas1,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = p2p_smem_bytes<W>();
   const void* fn = (const void*)k_relu_p2p<W>;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2P_TP, smem);
+  // odd widths stage a bool round byte-exactly in shared memory: up to 126 KB at w = 63
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2P_TP, smem);
   if (e != cudaSuccess) return e;
   // persistent cooperative grid: every CTA of the launch co-resident (the launch fails otherwise)
   const long long full = (long long)occ * sms;

@@ -131,3 +131,27 @@ def resnet_relu_config(model: ModelSpec, window: BitWindow | None = BitWindow(22
     """One window for every ReLU group (the 8-bit reduced ring (22,14) by default: |x| < 2^5 at f=16
     keeps the sign exact (Theorem 1), magnitudes below 2^-2 may be pruned (Theorem 2))."""
     return ReluConfig([window] * model.n_groups)
+
+
+def conv_macs(model: ModelSpec) -> int:
+    """Multiply-accumulates per sample of the model's conv and linear layers (residual branches
+    included): the dense contraction the int8-limb ring GEMMs compute (x 15 limb products)."""
+    from .nn import _layer_shape
+
+    total = 0
+
+    def visit(layers, cur):
+        nonlocal total
+        for L in layers:
+            nxt = _layer_shape(L, cur)
+            if isinstance(L, Conv2d):
+                total += nxt[0] * nxt[1] * nxt[2] * L.in_channels * L.kh * L.kw
+            elif isinstance(L, Linear):
+                total += L.in_features * L.out_features
+            elif isinstance(L, Residual):
+                visit(L.body, cur)
+                visit(L.shortcut, cur)
+            cur = nxt
+
+    visit(model.layers, tuple(model.input_shape))
+    return total
