@@ -66,8 +66,8 @@ def parse():
     p.add_argument("--workload", choices=["relu", "resnet18", "resnet50"], default="relu")
     p.add_argument("--batch", type=int, default=None, help="ResNet batch (default 512 / 128)")
     p.add_argument("--relu-config", default="search",
-                   help="ResNet per-group windows: 'search' = configs/<model>_windows_budget.json (the window "
-                        "search's result) when present, 'uniform' = (k, m) for every group, or a ReluConfig JSON path")
+                   help="ResNet per-group windows: 'search' = configs/<model>_windows_w8.json (8-bit windows at "
+                        "the window search's per-group k, tools/search_resnet.py) when present, 'uniform' = (k, m) for every group, or a ReluConfig JSON path")
     p.add_argument("--resnet-triple-gb", type=float, default=100.0,
                    help="HBM budget for one ResNet micro-batch's triples (both parties)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
@@ -424,7 +424,7 @@ def resnet_windows(args, model):
 
     path = args.relu_config
     if path == "search":
-        path = os.path.join(ROOT, "configs", f"{args.workload}_windows_budget.json")
+        path = os.path.join(ROOT, "configs", f"{args.workload}_windows_w8.json")
         if not os.path.exists(path):
             path = "uniform"
     if path == "uniform":

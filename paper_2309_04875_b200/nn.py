@@ -5,13 +5,18 @@ Same layer vocabulary, manifest JSON and semantics as the reference
 plus ``Residual`` (out = body(x) + shortcut(x)), which ResNets need and the
 reference lacks.  Every layer runs on the GPU:
 
-* Linear / Conv2d: ring-exact (X W^T) mod 2^64 on int8 tensor cores.  The share
-  is split into 8 byte limbs by a fused im2col kernel (hb_im2col_limbs), the
-  encoded weight into J balanced signed byte limbs (once per model), ONE int8
-  GEMM produces every limb product (cuBLASLt via torch._int_mm, s8 x s8 ->
-  s32), and hb_limb_combine folds the products mod 2^64 together with the local
-  truncation, the party-0 bias and the NCHW layout.  Bit-identical to the
-  reference's uint64 numpy matmul (nn.py:214-243).
+* Linear / Conv2d: ring-exact (X W^T) mod 2^64 on the int8 tensor cores, by
+  byte limbs: the share as 8 unsigned byte limbs, the encoded weight as J
+  balanced signed byte limbs (once per model); limb products with the same
+  byte shift accumulate in the same TMEM columns and the epilogue folds them
+  mod 2^64 together with the local truncation, the party-0 bias and an
+  optional fused residual add.  The path is the hand-written tcgen05 kernel:
+  hb_limbs_nhwc (NHWC limb planes) + hb_conv_limbs_tma (TMA-fed implicit GEMM)
+  for every ResNet geometry, small-K convs (the 3-channel stem) through
+  hb_im2col_planes on the same kernel, and the fused-gather tcgen05 kernel
+  hb_conv_limbs_tc for shapes neither TMA form tiles.  HB_RING_GEMM=cublaslt
+  (im2col + torch._int_mm + combine) is a cross-check only, as is J > 3.
+  Bit-identical to the reference's uint64 numpy matmul (nn.py:214-243).
 * AvgPool: hb_avgpool (window sum, * encode(1/kk), truncation; nn.py:246-259).
 * Relu: ``protocol.relu`` (one party, any endpoint) or, for both parties on one
   GPU, ``protocol.relu_pair`` (model_forward_pair / run_local_forward).

@@ -5,7 +5,11 @@
 Validation set: synthetic inputs of the benchmark shape; labels = the exact (full-window) model's
 argmax, so "accuracy" is agreement with the unreduced network (random-init weights: there is no
 dataset or checkpoint here).  Writes configs/<model>_windows_{eco,budget}.json (ReluConfig JSON +
-accuracy, baseline, bits fraction, search trace).
+accuracy, baseline, bits fraction, search trace) and configs/<model>_windows_w8.json, the benchmark's
+8-bit windows: per group k from the lossless eco search (the window's top bit covers the group's
+activation range, Theorem 1) and m = k - 8.  With random-init weights the exact model's argmax is
+nearly constant, so the budget search's accuracy criterion cannot tell windows apart (it keeps the
+smallest m or drops whole groups); the eco search's k does not depend on the labels.
 
     python tools/search_resnet.py resnet18 [--n 64] [--budget 1/8] [--widths 0,6,8]
 """
@@ -47,6 +51,12 @@ def main():
     eco = search.search_eco(model, x_val, labels, seed=a.seed)
     print(f"[search] eco {time.time() - t:.1f}s {json.dumps(eco.to_json())}", flush=True)
     eco.save(os.path.join(out_dir, f"{a.model}_windows_eco.json"))
+    w8 = {"groups": [{"k": w.k, "m": max(0, w.k - 8)} for w in eco.windows],
+          "search": {"kind": "search_eco k per group, m = k - 8", "seed": a.seed,
+                     "validation": f"{a.n} synthetic uniform[0,1) inputs of shape {shape}",
+                     "activation_ranges": {str(g): v for g, v in ranges.items()}}}
+    with open(os.path.join(out_dir, f"{a.model}_windows_w8.json"), "w") as fh:
+        json.dump(w8, fh, indent=2)
     t = time.time()
     widths = tuple(int(w) for w in a.widths.split(","))
     bud = search.search_budget(model, x_val, labels, a.budget, candidate_widths=widths, seed=a.seed)
