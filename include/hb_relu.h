@@ -248,6 +248,14 @@ int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height
                       int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
                       int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream);
 
+/* Both parties' convs of one layer in ONE launch (same geometry and weights; the pair of a 1-GPU
+ * time-sliced forward): party 0 on planes0 -> y0 (+ bias), party 1 on planes1 -> y1, each with its
+ * own truncation and optional residual.  Same results as two hb_conv_limbs_tma calls. */
+int hb_conv_limbs_tma_pair(const uint8_t* planes0, const uint8_t* planes1, int batch, int channels, int height,
+                           int width, int kh, int kw, int stride, int pad, const int8_t* wlimbs, int n_out,
+                           int j_limbs, int n_tile, int frac_bits, const uint64_t* bias, const uint64_t* residual0,
+                           const uint64_t* residual1, uint64_t* y0, uint64_t* y1, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,8 @@ _SIGS = {
     "hb_limbs_nhwc": (ctypes.c_int, [u64p] + [ctypes.c_int] * 4 + [u64p, ctypes.c_void_p]),
     "hb_conv_limbs_tma": (ctypes.c_int, [u64p] + [ctypes.c_int] * 8 + [u64p] + [ctypes.c_int] * 5 + [u64p, u64p, u64p,
                                                                                                  ctypes.c_void_p]),
+    "hb_conv_limbs_tma_pair": (ctypes.c_int, [u64p, u64p] + [ctypes.c_int] * 8 + [u64p] + [ctypes.c_int] * 4
+                               + [u64p] * 5 + [ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -624,9 +624,8 @@ int hb_im2col_planes(const uint64_t* x, int batch, int channels, int height, int
                      "hb_im2col_planes");
 }
 
-int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
-                      int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
-                      int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream) {
+static int hb_conv_check_tma(int batch, int channels, int height, int width, int kh, int kw, int stride, int pad,
+                             int j_limbs, int n_tile) {
   if (batch < 0 || channels <= 0 || height <= 0 || width <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0)
     return fail(HB_ERR_CONFIG, "bad conv geometry");
   if (height + 2 * pad < kh || width + 2 * pad < kw) return fail(HB_ERR_CONFIG, "kernel larger than padded input");
@@ -637,14 +636,43 @@ int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height
   if (j_limbs < 1 || j_limbs > 3) return fail(HB_ERR_CONFIG, "tensor-core path supports 1..3 weight limbs");
   if (n_tile != 16 && n_tile != 32 && n_tile != 64 && n_tile != 128)
     return fail(HB_ERR_CONFIG, "n_tile must be 16, 32, 64 or 128");
-  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
   int bb, bh, bw;
   const int oh = (height + 2 * pad - kh) / stride + 1, ow = (width + 2 * pad - kw) / stride + 1;
   if (hb_tma_conv_box(batch, oh, ow, &bb, &bh, &bw))
     return fail(HB_ERR_CONFIG, "output %dx%d does not tile into 128-pixel boxes", oh, ow);
-  return cuda_status(hb_tma_conv(planes, batch, channels, height, width, kh, kw, stride, pad, wlimbs, n_out, j_limbs,
-                                 n_tile, party, frac_bits, bias, residual, y, S(stream)),
+  return HB_OK;
+}
+
+int hb_conv_limbs_tma(const uint8_t* planes, int batch, int channels, int height, int width, int kh, int kw,
+                      int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs, int n_tile, int party,
+                      int frac_bits, const uint64_t* bias, const uint64_t* residual, uint64_t* y, void* stream) {
+  int rc = hb_conv_check_tma(batch, channels, height, width, kh, kw, stride, pad, j_limbs, n_tile);
+  if (rc) return rc;
+  if (party != 0 && party != 1) return fail(HB_ERR_CONFIG, "party must be 0 or 1, got %d", party);
+  const uint8_t* pl[1] = {planes};
+  const uint64_t* rs[1] = {residual};
+  uint64_t* ys[1] = {y};
+  return cuda_status(hb_tma_conv(1, pl, batch, channels, height, width, kh, kw, stride, pad, wlimbs, n_out, j_limbs,
+                                 n_tile, &party, frac_bits, bias, rs, ys, S(stream)),
                      "hb_conv_limbs_tma");
+}
+
+int hb_conv_limbs_tma_pair(const uint8_t* planes0, const uint8_t* planes1, int batch, int channels, int height,
+                           int width, int kh, int kw, int stride, int pad, const int8_t* wlimbs, int n_out, int j_limbs,
+                           int n_tile, int frac_bits, const uint64_t* bias, const uint64_t* residual0,
+                           const uint64_t* residual1, uint64_t* y0, uint64_t* y1, void* stream) {
+  if ((residual0 == nullptr) != (residual1 == nullptr))
+    return fail(HB_ERR_CONFIG, "residual0 / residual1 must both be given or both be NULL");
+  // the single-party entry point validates the geometry; run its checks once for party 0
+  int rc = hb_conv_check_tma(batch, channels, height, width, kh, kw, stride, pad, j_limbs, n_tile);
+  if (rc) return rc;
+  const uint8_t* pl[2] = {planes0, planes1};
+  const uint64_t* rs[2] = {residual0, residual1};
+  uint64_t* ys[2] = {y0, y1};
+  const int parties[2] = {0, 1};
+  return cuda_status(hb_tma_conv(2, pl, batch, channels, height, width, kh, kw, stride, pad, wlimbs, n_out, j_limbs,
+                                 n_tile, parties, frac_bits, bias, rs, ys, S(stream)),
+                     "hb_conv_limbs_tma_pair");
 }
 
 int hb_deal_triples(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int kind, int width,

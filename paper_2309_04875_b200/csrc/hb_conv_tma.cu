@@ -199,6 +199,7 @@ __device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t da0, uint64_
 template <int NT, int PASSES, int J>
 __global__ void __launch_bounds__(TMA_THREADS, 1)
     k_conv_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap8,
+               const __grid_constant__ CUtensorMap tmapB, const __grid_constant__ CUtensorMap tmap8B,
                const TmaConvArgs A) {
   using PS = Pass<PASSES>;
   constexpr int SPP = PS::SPP;
@@ -236,6 +237,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
   if (warp == PROD_WARP && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap8) : "memory");
+    if (A.tiles > A.tiles_pp) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmapB) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap8B) : "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -248,7 +253,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
-        const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+        const int pp = t >= A.tiles_pp ? 1 : 0, tl = t - pp * A.tiles_pp;
+        const int mt = tl / A.tiles_n, ntile = tl - mt * A.tiles_n;
+        const CUtensorMap* tm = pp ? &tmapB : &tmap;
+        const CUtensorMap* tm8 = pp ? &tmap8B : &tmap8;
         const long long m0 = (long long)mt * BM;
         const int b0 = (int)(m0 / S), rem = (int)(m0 - (long long)b0 * S);
         const int oh0 = rem / A.OW, ow0 = rem - (rem / A.OW) * A.OW;
@@ -269,9 +277,9 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             mbar_expect_tx(&bar_full[st], tx);
             const int w = ow0 * A.stride - A.pad + kj, h = oh0 * A.stride - A.pad + ki, bc = cc * A.B + b0;
             if (nl == 8)  // all limbs in one box (tmap8: box limb extent 8)
-              tma_load_5d(sA, &tmap8, 0, w, h, bc, 0, &bar_full[st]);
+              tma_load_5d(sA, tm8, 0, w, h, bc, 0, &bar_full[st]);
             else
-              for (int l = 0; l < nl; ++l) tma_load_5d(sA + l * TPLANE, &tmap, 0, w, h, bc, l0 + l, &bar_full[st]);
+              for (int l = 0; l < nl; ++l) tma_load_5d(sA + l * TPLANE, tm, 0, w, h, bc, l0 + l, &bar_full[st]);
             bulk_load(sA + a_limbs * TPLANE, wsrc + (long long)kb * bbytes, (uint32_t)bbytes, &bar_full[st]);
           }
         }
@@ -339,16 +347,20 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     int u = 0;
     long long e_wait = 0, e_read = 0, e_a = 0;  // dbg & 4 (warp 0): tfull waits, tfull -> tempty-arrive
     for (int t = blockIdx.x; t < A.tiles; t += gridDim.x) {
-      const int mt = t / A.tiles_n, ntile = t - mt * A.tiles_n;
+      const int pp = t >= A.tiles_pp ? 1 : 0, tl = t - pp * A.tiles_pp;
+      const int mt = tl / A.tiles_n, ntile = tl - mt * A.tiles_n;
+      const int party = A.party[pp];
+      const u64* __restrict__ res = A.res[pp];
+      u64* __restrict__ yout = A.y[pp];
       const long long em = (long long)mt * BM + quarter * 32 + lane;
       const bool eok = em < A.M;
       const int eb = eok ? (int)(em / S) : 0;
       const long long esp = eok ? em - (long long)eb * S : 0;
       const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-      if (A.res && eok && cgrp < NGRP)  // residual lines into L2 while the MMAs run
+      if (res && eok && cgrp < NGRP)  // residual lines into L2 while the MMAs run
         for (int c = cgrp * CPG; c < (cgrp + 1) * CPG; ++c)
           if (ntile * NT + c < A.N)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(A.res + ((long long)eb * A.N + ntile * NT + c) * S + esp));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(res + ((long long)eb * A.N + ntile * NT + c) * S + esp));
       if constexpr (PASSES == 1) {
         e_a = clock64();
         mbar_wait(&bar_tfull[0], u & 1);
@@ -383,10 +395,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
               const int n = ntile * NT + cb + k;
               if (n < A.N) {
                 const long long oi = ((long long)eb * A.N + n) * S + esp;
-                u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
-                if (A.party == 0 && A.bias) yv += A.bias[n];
-                if (A.res) yv += __ldg(reinterpret_cast<const unsigned long long*>(A.res + oi));  // add_shares
-                A.y[oi] = yv;
+                u64 yv = party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                if (party == 0 && A.bias) yv += A.bias[n];
+                if (res) yv += __ldg(reinterpret_cast<const unsigned long long*>(res + oi));  // add_shares
+                yout[oi] = yv;
               }
             }
           }
@@ -400,8 +412,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 8; ++k) {  // residual loads overlap the TMEM loads
               const int n = ntile * NT + c0 + k;
-              acc[k] = (A.res && eok && n < A.N) ? __ldg(reinterpret_cast<const unsigned long long*>(
-                                                        A.res + ((long long)eb * A.N + n) * S + esp))
+              acc[k] = (res && eok && n < A.N) ? __ldg(reinterpret_cast<const unsigned long long*>(
+                                                        res + ((long long)eb * A.N + n) * S + esp))
                                                   : 0ull;
             }
             tmem_wait_ld();
@@ -426,10 +438,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
               for (int k = 0; k < 8; ++k) {
                 const int n = ntile * NT + c0 + k;
                 if (n < A.N) {
-                  u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
-                  if (A.party == 0 && A.bias) yv += A.bias[n];
+                  u64 yv = party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                  if (party == 0 && A.bias) yv += A.bias[n];
                   yv += rsd[k];  // fused residual add (add_shares, sharing.py:118-122); 0 without one
-                  A.y[((long long)eb * A.N + n) * S + esp] = yv;
+                  yout[((long long)eb * A.N + n) * S + esp] = yv;
                 }
               }
             }
@@ -492,11 +504,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
               for (int k = 0; k < 8; ++k) {
                 const int n = ntile * NT + c0 + k;
                 if (n < A.N) {
-                  u64 yv = A.party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
-                  if (A.party == 0 && A.bias) yv += A.bias[n];
+                  u64 yv = party == 0 ? (acc[k] >> A.frac) : (0ull - ((0ull - acc[k]) >> A.frac));
+                  if (party == 0 && A.bias) yv += A.bias[n];
                   const long long oi = ((long long)eb * A.N + n) * S + esp;
-                  if (A.res) yv += __ldg(reinterpret_cast<const unsigned long long*>(A.res + oi));  // add_shares
-                  A.y[oi] = yv;
+                  if (res) yv += __ldg(reinterpret_cast<const unsigned long long*>(res + oi));  // add_shares
+                  yout[oi] = yv;
                 }
               }
             }
@@ -600,12 +612,13 @@ extern "C" int hb_debug_tma_stamps(long long* host, long long cap) {
   return (int)n;
 }
 
-cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int kh, int kw, int stride, int pad,
-                        const int8_t* wl, int N, int J, int nt, int party, int frac, const uint64_t* bias,
-                        const uint64_t* res, uint64_t* y, cudaStream_t s) {
+cudaError_t hb_tma_conv(int nparts, const uint8_t* const* planes, int B, int C, int H, int W, int kh, int kw,
+                        int stride, int pad, const int8_t* wl, int N, int J, int nt, const int* party, int frac,
+                        const uint64_t* bias, const uint64_t* const* res, uint64_t* const* y, cudaStream_t s) {
   using namespace hb::tc;
   auto encode = encode_fn();
   if (!encode) return cudaErrorNotSupported;
+  if (nparts != 1 && nparts != 2) return cudaErrorInvalidValue;
   TmaConvArgs A;
   A.OH = (H + 2 * pad - kh) / stride + 1;
   A.OW = (W + 2 * pad - kw) / stride + 1;
@@ -622,13 +635,17 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   A.B = B;
   A.nkb = kh * kw * A.ncc;
   A.tiles_n = (N + nt - 1) / nt;
-  A.tiles = (int)((A.M + BM - 1) / BM) * A.tiles_n;
+  A.tiles_pp = (int)((A.M + BM - 1) / BM) * A.tiles_n;
+  A.tiles = nparts * A.tiles_pp;
   A.wl = wl;
-  A.party = party;
   A.frac = frac;
   A.bias = bias;
-  A.res = res;
-  A.y = y;
+  for (int p = 0; p < 2; ++p) {
+    const int q = p < nparts ? p : 0;
+    A.party[p] = party[q];
+    A.res[p] = res[q];
+    A.y[p] = y[q];
+  }
   static const int dbg = [] {
     const char* e = getenv("HB_TC_DEBUG");
     return e ? atoi(e) : 0;
@@ -648,25 +665,29 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
 
   // planes [limb][C/64][B][H][W][64] uint8 as 5-D (64 channels, W, H, chunk*B + b, limb); box
   // (64, bw*stride, bh*stride, bb, 1 limb), traversal stride = conv stride
-  CUtensorMap tmap;
   const cuuint64_t dims[5] = {(cuuint64_t)TKB, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B * (C / TKB), 8};
   const cuuint64_t strides[4] = {(cuuint64_t)TKB, (cuuint64_t)W * TKB, (cuuint64_t)H * W * TKB,
                                  (cuuint64_t)B * H * W * C};
   const cuuint32_t box[5] = {(cuuint32_t)TKB, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bb, 1};
+  const cuuint32_t box8[5] = {box[0], box[1], box[2], box[3], 8};
   const cuuint32_t estr[5] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1, 1};
   if (box[1] > 256 || box[2] > 256) return cudaErrorInvalidValue;
-  CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, TKB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (TKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  CUtensorMap tmap8;
-  const cuuint32_t box8[5] = {box[0], box[1], box[2], box[3], 8};
-  r = encode(&tmap8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes), dims, strides, box8, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE,
-             TKB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (TKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  // per sub-problem: one map with a 1-limb box (passes that load a limb range) and one with all 8
+  CUtensorMap tmap[2], tmap8[2];
+  for (int p = 0; p < nparts; ++p) {
+    for (int all = 0; all < 2; ++all) {
+      CUresult r = encode(all ? &tmap8[p] : &tmap[p], CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(planes[p]),
+                          dims, strides, all ? box8 : box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          TKB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                    : (TKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  if (nparts == 1) {
+    tmap[1] = tmap[0];
+    tmap8[1] = tmap8[0];
+  }
   const int grid = A.tiles < sm_count() ? A.tiles : sm_count();
   cudaError_t e;
   A.stamps = nullptr;
@@ -680,7 +701,7 @@ cudaError_t hb_tma_conv(const uint8_t* planes, int B, int C, int H, int W, int k
   if (nt == NT_ && J == J_) {                                                                                    \
     e = cudaFuncSetAttribute(k_conv_tma<NT_, P_, J_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                              \
-    k_conv_tma<NT_, P_, J_><<<grid, TMA_THREADS, smem, s>>>(tmap, tmap8, A);                                     \
+    k_conv_tma<NT_, P_, J_><<<grid, TMA_THREADS, smem, s>>>(tmap[0], tmap8[0], tmap[1], tmap8[1], A);            \
     return cudaGetLastError();                                                                                   \
   }
 #define HB_NT(NT_, P_) HB_NTJ(NT_, P_, 1) HB_NTJ(NT_, P_, 2) HB_NTJ(NT_, P_, 3)

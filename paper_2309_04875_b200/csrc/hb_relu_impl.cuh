@@ -126,20 +126,18 @@ struct PairGeo {
 #ifndef HB_PAIR_MINB
 #define HB_PAIR_MINB 1
 #endif
+// One group of both parties' elements through every round: thread t of party `party` owns the GS
+// elements starting at layer element e0 (`valid` of them in the layer); the peer thread (t of the
+// other half of the CTA) owns the same elements.  Returns the output share (or the DReLU share when
+// drelu_only) in `out`; every thread of the CTA must call it (it holds the exchange barriers).
 template <int W, int TP, bool RING64>
-__global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairArgs A) {
+HB_DEV void pair_group(const PairArgs& A, const int party, const int t, const u64 e0, const int valid,
+                       u64* __restrict__ wire, u64 (&out)[Geo<W>::GS]) {
   using G = Geo<W>;
   using K = Kit<W>;
   constexpr int GS = G::GS, PW = G::PW, SEGW = PairGeo<W>::SEGW, L = K::L, NSEG = 1 + 2 * L;
-  extern __shared__ u64 wire[];  // [buf 2][party 2][SEGW][TP]
-
-  const int party = threadIdx.x >= TP ? 1 : 0;
-  const int t = threadIdx.x - party * TP;
   const bool p0 = party == 0;
   const u64 n = A.n;
-  const u64 end = A.first + A.count;
-  const u64 e0 = A.first + ((u64)blockIdx.x * TP + t) * GS;
-  const int valid = e0 >= end ? 0 : (int)min((u64)GS, end - e0);
   const PartyIO& io = A.io[party];
   const u64 MN = RING64 ? ~0ull : nmask(A.N);  // Z/2^64: masks fold away at compile time
   const bool mult = !A.drelu_only;
@@ -236,14 +234,15 @@ __global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairAr
     }
   }
   if (!mult) {
-    store_u64s<GS>(io.y + e0, valid, d);
+#pragma unroll
+    for (int j = 0; j < GS; ++j) out[j] = d[j];
     return;
   }
 
   // ---- round L+2: y = MUL(x, d)
   {
     const int buf = L & 1;
-    u64 e2[GS], f2[GS], yv[GS];
+    u64 e2[GS], f2[GS];
 #pragma unroll
     for (int j = 0; j < GS; ++j) {
       e2[j] = (x[j] - a2[j]) & MN;
@@ -256,10 +255,23 @@ __global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairAr
     for (int j = 0; j < GS; ++j) {
       const u64 E = (e2[j] + slot(buf, party ^ 1, j)) & MN;
       const u64 F = (f2[j] + slot(buf, party ^ 1, GS + j)) & MN;
-      yv[j] = mul_z(p0, E, F, a2[j], b2[j], c2[j], MN);
+      out[j] = mul_z(p0, E, F, a2[j], b2[j], c2[j], MN);
     }
-    store_u64s<GS>(io.y + e0, valid, yv);
   }
+}
+
+template <int W, int TP, bool RING64>
+__global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairArgs A) {
+  constexpr int GS = Geo<W>::GS;
+  extern __shared__ u64 wire[];  // [buf 2][party 2][SEGW][TP]
+  const int party = threadIdx.x >= TP ? 1 : 0;
+  const int t = threadIdx.x - party * TP;
+  const u64 end = A.first + A.count;
+  const u64 e0 = A.first + ((u64)blockIdx.x * TP + t) * GS;
+  const int valid = e0 >= end ? 0 : (int)min((u64)GS, end - e0);
+  u64 yv[GS];
+  pair_group<W, TP, RING64>(A, party, t, e0, valid, wire, yv);
+  store_u64s<GS>(A.io[party].y + e0, valid, yv);
 }
 
 // ------------------------------------------------------------------ staged (one party per launch)

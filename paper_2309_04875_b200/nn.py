@@ -457,6 +457,34 @@ def _conv_dev(d, lay, L: Conv2d, lw, party, frac, residual=None):
     return _gemm_cublaslt(d, geom, lw, party, frac, 1), "nchw"
 
 
+# both parties' convs of a layer in one launch (hb_conv_limbs_tma_pair) in model_forward_pair;
+# HB_CONV_PAIR=0 launches them one by one
+CONV_PAIR = os.environ.get("HB_CONV_PAIR", "1") != "0"
+
+
+def _conv_pair_dev(ds, lay, L: Conv2d, lw, parties, frac, residuals=None):
+    """Both parties' TMA convs of one layer in ONE launch; None when the layer does not qualify
+    (then the caller runs _conv_dev per party).  Same shares as two _conv_dev calls."""
+    if not (CONV_PAIR and len(ds) == 2 and tuple(parties) == (0, 1) and _use_tc(lw)):
+        return None
+    geom = (L.kh, L.kw, L.stride, L.pad)
+    xs = [_to_layout(d, lay, "nchw") for d in ds]
+    if xs[0].shape != xs[1].shape or not _tma_ok(xs[0], geom, lw):
+        return None
+    b, c, h, w = xs[0].shape
+    oh, ow = (h + 2 * L.pad - L.kh) // L.stride + 1, (w + 2 * L.pad - L.kw) // L.stride + 1
+    outs = [torch.empty((b, lw.n, oh, ow), dtype=torch.int64, device=xs[0].device) for _ in xs]
+    if residuals is not None and any(r.shape != outs[0].shape for r in residuals):
+        return None
+    s = _dev.stream_handle()
+    planes = [_limb_planes(x, s) for x in xs]
+    res = [None, None] if residuals is None else [r.contiguous().data_ptr() for r in residuals]
+    _lib.call("hb_conv_limbs_tma_pair", planes[0].data_ptr(), planes[1].data_ptr(), b, c, h, w, L.kh, L.kw, L.stride,
+              L.pad, lw.wl_tma.data_ptr(), lw.n, lw.j, lw.nt_tma, frac, lw.bias.data_ptr(), res[0], res[1],
+              outs[0].data_ptr(), outs[1].data_ptr(), s)
+    return outs
+
+
 def _linear_dev(d, lw, party, frac):
     b, k = d.shape
     if _use_tc(lw):
@@ -590,7 +618,10 @@ def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_me
                     h = [_to_layout(y, lh, "nchw") for y in h]
                     lw = _weight(model.weights[last.weight], model.weights[last.bias], cfg)
                     geom = (last.kh, last.kw, last.stride, last.pad)
-                    if _use_tc(lw) and _tma_ok(a[0], geom, lw) and all(
+                    pair = _conv_pair_dev(a, "nchw", last, lw, parties, cfg.frac_bits, h)
+                    if pair is not None:
+                        ds = pair
+                    elif _use_tc(lw) and _tma_ok(a[0], geom, lw) and all(
                             y.shape == _conv_out_shape(d, last) for d, y in zip(a, h)):
                         ds = [_conv_dev(d, "nchw", last, lw, p, cfg.frac_bits, y)[0] for d, p, y in zip(a, parties, h)]
                     else:
@@ -604,8 +635,12 @@ def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_me
                     lay = la
             elif isinstance(L, Conv2d):
                 lw = _weight(model.weights[L.weight], model.weights[L.bias], cfg)
-                res = [_conv_dev(d, lay, L, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]
-                ds, lay = [r[0] for r in res], res[0][1]
+                pair = _conv_pair_dev(ds, lay, L, lw, parties, cfg.frac_bits)
+                if pair is not None:
+                    ds, lay = pair, "nchw"
+                else:
+                    res = [_conv_dev(d, lay, L, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]
+                    ds, lay = [r[0] for r in res], res[0][1]
             elif isinstance(L, Linear):
                 lw = _weight(model.weights[L.weight], model.weights[L.bias], cfg)
                 ds = [_linear_dev(d, lw, p, cfg.frac_bits) for d, p in zip(ds, parties)]

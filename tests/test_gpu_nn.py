@@ -236,3 +236,34 @@ def test_fused_residual_block_at_layer3_layer4_geometry(cin, cout, side):
     want, _, _ = ON.run_local_forward(layers, model.input_shape, model.weights, [(22, 14)], x_f, 5)
     logits, _, _, _ = nn.run_local_forward(model, cfg, x_f, 5, pair=True, layer_logs=False)
     assert np.array_equal(logits, want)
+
+
+@pytest.mark.parametrize("model,batch,geom", _conv_cases())
+def test_every_resnet_conv_pair_launch_bit_exact(model, batch, geom):
+    """Both parties' convs of a layer in ONE launch (hb_conv_limbs_tma_pair: party 0 and party 1
+    tiles on one persistent grid, each with its own tensor maps, truncation, bias and residual)
+    equal the reference conv per party -- plus the residual share when one is fused."""
+    cin, cout, k, stride, pad, h, w, wname, bname = geom
+    if cin % 64:
+        pytest.skip("the stem runs through im2col planes, one launch per party")
+    rng = np.random.default_rng(cin * 7 + cout + h)
+    xs = [np.frombuffer(rng.bytes(8 * batch * cin * h * w), dtype="<u8").copy().reshape(batch, cin, h, w)
+          for _ in range(2)]
+    wt, bias = model.weights[wname], model.weights[bname] + np.float32(0.01)
+    layer = nn.Conv2d(cin, cout, k, k, stride, pad, weight="w", bias="b")
+    lw = nn._weight(wt, bias, FixedPointConfig())
+    want = [ON.conv2d(x, p, cin, cout, k, k, stride, pad, wt, bias) for p, x in enumerate(xs)]
+    ds = [torch.from_numpy(x.view(np.int64)).cuda() for x in xs]
+    for fused in (False, True):
+        res = None
+        if fused:
+            res = [torch.from_numpy(rng.integers(0, 2**63, want[0].shape, dtype=np.uint64).view(np.int64)).cuda()
+                   for _ in range(2)]
+        nn._PLANES.clear()
+        out = nn._conv_pair_dev(ds, "nchw", layer, lw, (0, 1), 16, res)
+        assert out is not None
+        for p in (0, 1):
+            got = out[p].cpu().numpy().view(np.uint64)
+            exp = want[p] if res is None else want[p] + res[p].cpu().numpy().view(np.uint64)
+            assert np.array_equal(got, exp), (geom, p, fused)
+    nn._PLANES.clear()
