@@ -68,6 +68,8 @@ def parse():
     p.add_argument("--relu-config", default="search",
                    help="ResNet per-group windows: 'search' = configs/<model>_windows_w8.json (8-bit windows at "
                         "the window search's per-group k, tools/search_resnet.py) when present, 'uniform' = (k, m) for every group, or a ReluConfig JSON path")
+    p.add_argument("--no-model-graph", action="store_true",
+                   help="ResNet: launch the forward's kernels one by one instead of replaying it as one CUDA graph")
     p.add_argument("--resnet-triple-gb", type=float, default=100.0,
                    help="HBM budget for one ResNet micro-batch's triples (both parties)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
@@ -503,12 +505,28 @@ def run_resnet(args):
     for _ in range(args.warmup):
         y0, y1 = fwd()
     torch.cuda.synchronize()
+    graph = None
+    if not args.no_model_graph:
+        # the whole forward (every micro-batch, both parties: ~110 kernels) as ONE CUDA graph: the same
+        # kernels on the same buffers, without the host's per-launch gaps between them
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            y0, y1 = fwd()
+        graph.replay()
+        torch.cuda.synchronize()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+            return y0, y1
+        return fwd()
+
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         a.record(s)
         for _ in range(args.steps):
-            y0, y1 = fwd()
+            y0, y1 = step()
         b.record(s)
         torch.cuda.synchronize()
     ms = a.elapsed_time(b) / args.steps
@@ -531,6 +549,7 @@ def run_resnet(args):
                                f"ReLU windows {cfg_desc}", "batch": batch,
                    "relu_elements_per_forward": relu_elems, "parties": "1 pair time-sliced on 1 GPU",
                    "micro_batch": mb, "stem": "CIFAR-style 3x3 stride 1, no maxpool",
+                   "cuda_graph": graph is not None,
                    "path": "nn.model_forward_pair: int8-limb ring conv ("
                            + ("hand-written tcgen05 kernel" if nn.RING_GEMM == "tc" else "cuBLASLt") + ") + fused pair ReLU kernel",
                    "weights": "random init (torchvision scheme), BN folded", "parallelism": "pair"},

@@ -86,16 +86,18 @@ struct P2PGeo {
   static constexpr __host__ __device__ u64 packet(int r) { return nseg(r) * (r <= L ? SB : SA); }
   static_assert(SB % 16 == 0 && SA % 16 == 0, "segments stay 16-byte aligned");
   // resident CTAs per SM the register budget is set for, and whether the exchange warms L2 with
-  // the next round's inputs (helps the wide rounds; measured, tools/micro/p2p_bench)
+  // the next round's inputs (helps the wide rounds only).  Measured on B200 with tools/micro/p2p_bench
+  // (both parties on one GPU, 2^24): w = 6: 5 CTAs, no prefetch (1.06e10 elem/s); w = 16 / 32: 6 CTAs,
+  // no prefetch (8.6e9 / 4.9e9, vs 8.5e9 / 4.3e9 at 5 / 4 CTAs); w = 64: 4 CTAs + prefetch (0.97 of H).
 #ifdef HB_P2P_MINB
   static constexpr int MINB = HB_P2P_MINB;
 #else
-  static constexpr int MINB = W <= 16 ? 5 : 4;
+  static constexpr int MINB = W <= 8 ? 5 : (W <= 32 ? 6 : 4);
 #endif
 #ifdef HB_P2P_PF
   static constexpr bool PF = HB_P2P_PF;
 #else
-  static constexpr bool PF = W > 16;
+  static constexpr bool PF = W > 32;
 #endif
 };
 

@@ -38,6 +38,7 @@ def main():
     p.add_argument("--widths", default="0,6,8")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--out-dir", default=os.path.join(ROOT, "configs"))
+    p.add_argument("--eco-only", action="store_true", help="skip the budget search")
     a = p.parse_args()
     model = models.resnet18_cifar(0) if a.model == "resnet18" else models.resnet50(0)
     shape = (3, 32, 32) if a.model == "resnet18" else (3, 64, 64)
@@ -57,6 +58,8 @@ def main():
                      "activation_ranges": {str(g): v for g, v in ranges.items()}}}
     with open(os.path.join(out_dir, f"{a.model}_windows_w8.json"), "w") as fh:
         json.dump(w8, fh, indent=2)
+    if a.eco_only:
+        return
     t = time.time()
     widths = tuple(int(w) for w in a.widths.split(","))
     bud = search.search_budget(model, x_val, labels, a.budget, candidate_widths=widths, seed=a.seed)
