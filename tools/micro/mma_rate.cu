@@ -66,12 +66,20 @@ void run(const char* name, double macs_per_iter) {
   cudaFuncSetAttribute(k_mma<PAT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int iters = 2000;
   k_mma<PAT, N><<<148, 128, 200 * 1024>>>(10, d);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
   k_mma<PAT, N><<<148, 128, 200 * 1024>>>(iters, d);
+  cudaEventRecord(e1);
   cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
   long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
-  printf("%-40s %8.1f clk per 8-MMA group  -> %6.0f MAC/clk/SM (peak 8192)  %s\n", name, avg / iters,
-         macs_per_iter / (avg / iters), cudaGetErrorString(cudaGetLastError()));
+  printf("%-40s %8.1f clk per 8-MMA group  -> %6.0f MAC/clk/SM (peak 8192)  %.2f int8 POPS (wall)  %s\n", name,
+         avg / iters, macs_per_iter / (avg / iters), 2.0 * 148 * iters * macs_per_iter / (ms * 1e-3) / 1e15,
+         cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
