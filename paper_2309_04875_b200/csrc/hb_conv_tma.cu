@@ -651,11 +651,7 @@ cudaError_t hb_tma_conv(int nparts, const uint8_t* const* planes, int B, int C, 
     return e ? atoi(e) : 0;
   }();
   A.dbg = dbg;
-  static const bool p2d = [] {  // double-buffered two-pass NT=64 (measured slower; experiments only)
-    const char* e = getenv("HB_TMA_P2D");
-    return e && atoi(e);
-  }();
-  const int passes = nt == 128 || (nt == 64 && p2d) ? 2 : 1;
+  const int passes = nt == 128 ? 2 : 1;
   const int stage_bytes = (passes == 1 ? 8 : J + 3) * TPLANE + J * nt * TKB;
   if (stage_bytes % 256) return cudaErrorInvalidValue;  // swizzle atoms stay aligned
   int ns = (227 * 1024 - 1024) / stage_bytes;
@@ -707,9 +703,6 @@ cudaError_t hb_tma_conv(int nparts, const uint8_t* const* planes, int B, int C, 
 #define HB_NT(NT_, P_) HB_NTJ(NT_, P_, 1) HB_NTJ(NT_, P_, 2) HB_NTJ(NT_, P_, 3)
   HB_NT(16, 1)
   HB_NT(32, 1)
-  if (passes == 2) {
-    HB_NT(64, 2)
-  }
   HB_NT(64, 1)
   HB_NT(128, 2)
 #undef HB_NT

@@ -374,9 +374,11 @@ def _tma_box(oh: int, ow: int):
 def _tma_box_ok(oh: int, ow: int, stride: int = 1) -> bool:
     """Mirror of every geometry check hb_tma_conv makes before encoding its tensor maps: the box
     tiles the output, and the input window it reads (box extent x conv stride) is at most 256 per
-    dimension (hb_conv_tma.cu:655-657); the traversal stride is at most 8."""
+    dimension (hb_conv_tma.cu box check); the traversal stride is at most 8 and the output width at
+    most 256 (hb_conv_limbs_tma's checks, hb_api.cu)."""
     box = _tma_box(oh, ow)
-    return box is not None and stride <= 8 and box[2] * stride <= 256 and box[1] * stride <= 256
+    return (box is not None and stride <= 8 and ow <= 256 and box[2] * stride <= 256
+            and box[1] * stride <= 256)
 
 
 def _tma_ok(x_nchw: torch.Tensor, geom, lw: _LimbWeight) -> bool:

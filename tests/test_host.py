@@ -276,3 +276,16 @@ def test_bench_self_launches_n_ranks():
     assert len(lines) == 1
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["rank_sum"] == 3 and rec["party_of_rank"] == [0, 1]
+
+
+def test_tma_geometry_mirror_matches_the_c_checks():
+    """nn._tma_box_ok accepts exactly the output geometries hb_conv_limbs_tma accepts, so a conv the
+    C side would reject falls back to the gather kernel instead of raising (advisor, round 1)."""
+    from paper_2309_04875_b200 import nn
+
+    assert nn._tma_box_ok(32, 32) and nn._tma_box_ok(4, 4, 2) and nn._tma_box_ok(1, 128)
+    assert not nn._tma_box_ok(1, 384)          # OW > 256
+    assert not nn._tma_box_ok(64, 128, 3)      # box width 128 x stride 3 > 256
+    assert not nn._tma_box_ok(8, 64, 5)        # 64 x 5 > 256
+    assert not nn._tma_box_ok(7, 7)            # 49 pixels do not tile 128
+    assert not nn._tma_box_ok(16, 16, 9)       # traversal stride > 8
