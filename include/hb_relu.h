@@ -80,6 +80,16 @@ int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, in
                        hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
                        int drelu_only, void* stream);
 
+/* Same ReLU with the shares in (pinned) HOST memory: x_p are read from and y_p written to host
+ * buffers, pipelined over three internal streams -- host-to-device copies, the fused kernel on
+ * element ranges, device-to-host copies -- in chunks of `chunk` elements (ramped at both ends), so
+ * both PCIe directions and the kernel overlap.  scratch: 4n uint64 of device memory.  Returns when
+ * y0 / y1 are complete.  Same shares, triples and rounds as hb_relu_pair. */
+int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx0, const uint64_t* hx1,
+                      uint64_t* hy0, uint64_t* hy1, hb_triples_t bool0, hb_triples_t bool1,
+                      hb_triples_t arith0, hb_triples_t arith1, int drelu_only, int64_t chunk,
+                      uint64_t* scratch, void* stream);
+
 /* ---- one party, staged: protocol.relu / protocol.drelu (protocol.py:179-199)
  * split at its exchanges.  Call round r = 0 .. hb_relu_rounds(): round r writes
  * this party's payload of round r into `own` (hb_relu_round_bytes bytes, except

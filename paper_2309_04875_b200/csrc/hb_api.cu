@@ -7,7 +7,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hb_relu.h"
 #include "hb_relu_impl.cuh"
@@ -248,6 +252,95 @@ int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, in
   A.m = m;
   A.drelu_only = drelu_only ? 1 : 0;
   return cuda_status(pair_dispatch(w, A, S(stream)), "hb_relu_pair");
+}
+
+// Per-device streams and events of the pinned-host pipeline (created once, reused by every call).
+struct HostPipe {
+  cudaStream_t in = nullptr, k = nullptr, out = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+static HostPipe& host_pipe(int dev, size_t nev) {
+  static std::mutex mu;
+  static std::map<int, HostPipe> pipes;
+  std::lock_guard<std::mutex> g(mu);
+  HostPipe& p = pipes[dev];
+  if (!p.in) {
+    cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p.k, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking);
+  }
+  while (p.ev.size() < nev) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    p.ev.push_back(e);
+  }
+  return p;
+}
+
+int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx0, const uint64_t* hx1, uint64_t* hy0,
+                      uint64_t* hy1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0, hb_triples_t arith1,
+                      int drelu_only, int64_t chunk, uint64_t* scratch, void* stream) {
+  if (n < 0 || chunk <= 0) return fail(HB_ERR_CONFIG, "bad element count or chunk");
+  if (n == 0)
+    return hb_relu_pair_range(ring_bits, k, m, n, 0, 0, nullptr, nullptr, nullptr, nullptr, bool0, bool1, arith0,
+                              arith1, drelu_only, stream);
+  if (!hx0 || !hx1 || !hy0 || !hy1 || !scratch) return fail(HB_ERR_CONFIG, "missing host buffer or scratch");
+  // chunk schedule: `chunk` elements in the middle, ramping from chunk/8 at both ends (shorter
+  // pipeline fill and drain)
+  std::vector<std::pair<int64_t, int64_t>> ch;  // (first, count)
+  {
+    int64_t left = n;
+    std::vector<int64_t> head, mid, tail;
+    for (int s = 3; s >= 1 && left > 0; --s) {
+      const int64_t c = std::min<int64_t>(std::max<int64_t>(chunk >> s, 1), left);
+      head.push_back(c);
+      left -= c;
+    }
+    for (int s = 3; s >= 1 && left > chunk; --s) {
+      const int64_t c = std::max<int64_t>(chunk >> s, 1);
+      tail.push_back(c);
+      left -= c;
+    }
+    while (left > 0) {
+      mid.push_back(std::min(chunk, left));
+      left -= mid.back();
+    }
+    int64_t lo = 0;
+    for (int64_t c : head) ch.push_back({lo, c}), lo += c;
+    for (int64_t c : mid) ch.push_back({lo, c}), lo += c;
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) ch.push_back({lo, *it}), lo += *it;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  HostPipe& P = host_pipe(dev, 2 * ch.size() + 2);
+  uint64_t *d0 = scratch, *d1 = scratch + n, *e0 = scratch + 2 * n, *e1 = scratch + 3 * n;
+  cudaEvent_t start = P.ev[2 * ch.size()], done = P.ev[2 * ch.size() + 1];
+  // the scratch and the triples are ordered on the caller's stream
+  cudaError_t e = cudaEventRecord(start, S(stream));
+  for (cudaStream_t st : {P.in, P.k, P.out})
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, start, 0);
+  if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host");
+  for (size_t i = 0; i < ch.size(); ++i) {
+    const int64_t lo = ch[i].first, c = ch[i].second;
+    cudaEvent_t copied = P.ev[2 * i], computed = P.ev[2 * i + 1];
+    e = cudaMemcpyAsync(d0 + lo, hx0 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d1 + lo, hx1 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
+    if (e == cudaSuccess) e = cudaEventRecord(copied, P.in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P.k, copied, 0);
+    if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host H2D");
+    const int rc = hb_relu_pair_range(ring_bits, k, m, n, lo, c, d0, d1, e0, e1, bool0, bool1, arith0, arith1,
+                                      drelu_only, P.k);
+    if (rc) return rc;
+    e = cudaEventRecord(computed, P.k);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P.out, computed, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hy0 + lo, e0 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hy1 + lo, e1 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
+    if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host D2H");
+  }
+  e = cudaEventRecord(done, P.out);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(S(stream), done, 0);
+  if (e == cudaSuccess) e = cudaEventSynchronize(done);  // the host outputs are complete on return
+  return cuda_status(e, "hb_relu_pair_host");
 }
 
 uint64_t hb_relu_p2p_bytes(int k, int m, int64_t n, int drelu_only, int64_t* ntiles) {

@@ -354,41 +354,19 @@ def relu_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: BitW
     return (_wrap(ArithShareTensor, 0, N, y0, x0.data, x0.shape), _wrap(ArithShareTensor, 1, N, y1, x1.data, x1.shape))
 
 
-_PIPE: dict = {}
-_PIPE_CHUNK = int(os.environ.get("HB_PIPE_CHUNK", str(1 << 21)))  # elements per pinned-pipeline chunk
+_PIPE_CHUNK = int(os.environ.get("HB_PIPE_CHUNK", str(1 << 21)))  # elements per pinned-pipeline chunk (2^19..2^22 measured: 2^21 best)
 
 
 def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=None):
-    """Pinned host shares in/out, pipelined over three dedicated streams -- host-to-device copies,
-    the fused kernel, device-to-host copies -- joined per chunk by events, so each copy engine is
-    fed back to back (PCIe is full duplex) and no copy waits behind one of the other direction.
-    Same kernel, same triples, same shares as the one-shot path."""
+    """Pinned host shares in/out: hb_relu_pair_host pipelines host-to-device copies, the fused
+    kernel on element ranges and device-to-host copies over three native streams joined per chunk
+    by events (chunks ramped at both ends), so both PCIe directions and the kernel overlap.  Same
+    kernel, same triples, same shares as the one-shot path."""
     dev = _dev.device()
-    chunk = chunk or _PIPE_CHUNK
-    if dev.index not in _PIPE:
-        _PIPE[dev.index] = tuple(torch.cuda.Stream() for _ in range(3))
-    s_in, s_k, s_out = _PIPE[dev.index]
     h0, h1 = x0.data.reshape(-1), x1.data.reshape(-1)
-    d0, d1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
-    e0, e1 = torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev)
     o0, o1 = torch.empty(n, dtype=torch.int64, pin_memory=True), torch.empty(n, dtype=torch.int64, pin_memory=True)
-    cur = torch.cuda.current_stream()
-    for st in (s_in, s_k, s_out):
-        st.wait_stream(cur)
-    lib = _lib.load()
-    tv = (views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi())  # same for every chunk
-    fn = lib.hb_relu_pair_range
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        with torch.cuda.stream(s_in):
-            d0[lo:hi].copy_(h0[lo:hi], non_blocking=True)
-            d1[lo:hi].copy_(h1[lo:hi], non_blocking=True)
-        s_k.wait_stream(s_in)
-        _lib.check(fn(N, window.k, window.m, n, lo, hi - lo, d0.data_ptr(), d1.data_ptr(), e0.data_ptr(),
-                      e1.data_ptr(), *tv, int(drelu_only), s_k.cuda_stream))
-        s_out.wait_stream(s_k)
-        with torch.cuda.stream(s_out):
-            o0[lo:hi].copy_(e0[lo:hi], non_blocking=True)
-            o1[lo:hi].copy_(e1[lo:hi], non_blocking=True)
-    s_out.synchronize()
+    scratch = torch.empty(4 * n, dtype=torch.int64, device=dev)
+    _lib.call("hb_relu_pair_host", N, window.k, window.m, n, h0.data_ptr(), h1.data_ptr(), o0.data_ptr(),
+              o1.data_ptr(), views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),
+              int(drelu_only), int(chunk or _PIPE_CHUNK), scratch.data_ptr(), _stream())
     return (ArithShareTensor(0, N, o0.reshape(x0.shape)), ArithShareTensor(1, N, o1.reshape(x1.shape)))

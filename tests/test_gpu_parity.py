@@ -328,3 +328,35 @@ def test_gpu_drelu_from_shares_and_sim_relu():
     t0, t1 = sharing.share_arith(e2, 64, np.random.default_rng(6))
     ref_keep = O.drelu_from_shares(t0.data, t1.data, 64, 20, 6)
     assert np.array_equal(out != 0.0, (ref_keep == 1) & (xf != 0.0))
+
+
+@pytest.mark.parametrize("n,chunk", [((1 << 22) + 12345, 1 << 20), ((1 << 22) + 7, 1 << 19)])
+def test_relu_pair_pinned_host_pipeline(n, chunk, monkeypatch):
+    """relu_pair on PINNED HOST shares (> 2^22 elements) runs the native pipeline hb_relu_pair_host
+    -- H2D / kernel on element ranges / D2H over three streams, ramped chunks, a partial last chunk --
+    and returns host shares equal to the device path's on the same triples, with the same meters."""
+    from paper_2309_04875_b200 import dealer
+
+    monkeypatch.setattr(protocol, "_PIPE_CHUNK", chunk)
+    k, m = 22, 14
+    w, L = k - m, protocol.prefix_levels(k - m)
+    rng = np.random.default_rng(n)
+    x = [rng.integers(0, 2**63, n, dtype=np.uint64) for _ in range(2)]
+    outs = []
+    for pinned in (False, True):
+        eps = transport.local_pair()
+        stores = (dealer.TripleStore(0), dealer.TripleStore(1))
+        dealer.stock_on_device(stores, (0, 1), dealer.BOOL, w, n * (1 + 2 * L), seed=3)
+        dealer.stock_on_device(stores, (0, 1), dealer.ARITH, 64, 2 * n, seed=4)
+        sess = (protocol.ProtocolSession(eps[0], stores[0]), protocol.ProtocolSession(eps[1], stores[1]))
+        ts = [torch.from_numpy(v.view(np.int64)) for v in x]
+        ts = [t.pin_memory() for t in ts] if pinned else [t.cuda() for t in ts]
+        r0, r1 = protocol.relu_pair(sess, ArithShareTensor(0, 64, ts[0]), ArithShareTensor(1, 64, ts[1]), BitWindow(k, m))
+        if pinned:
+            assert not r0.data.is_cuda
+        outs.append(([np.asarray(r.data.cpu() if isinstance(r.data, torch.Tensor) else r.data).view(np.uint64)
+                      for r in (r0, r1)], eps[0].meter.to_json()))
+    assert np.array_equal(outs[0][0][0], outs[1][0][0]) and np.array_equal(outs[0][0][1], outs[1][0][1])
+    assert outs[0][1] == outs[1][1]
+    want = O.ring_mul(O.ring_add(x[0], x[1], 64), O.drelu_from_shares(x[0], x[1], 64, k, m), 64)
+    assert np.array_equal(O.ring_add(outs[1][0][0], outs[1][0][1], 64), want)

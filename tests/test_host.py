@@ -289,3 +289,5 @@ def test_tma_geometry_mirror_matches_the_c_checks():
     assert not nn._tma_box_ok(8, 64, 5)        # 64 x 5 > 256
     assert not nn._tma_box_ok(7, 7)            # 49 pixels do not tile 128
     assert not nn._tma_box_ok(16, 16, 9)       # traversal stride > 8
+
+
