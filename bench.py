@@ -269,6 +269,9 @@ def run_single(args):
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    from paper_2309_04875_b200 import _dev as _hb_dev
+
+    _hb_dev.bind_thread()  # the library's own CUDA runtime on this rank's device
     n, k, m, N = 1 << args.logn, args.k, args.m, args.ring_bits
     w = k - m
     L = protocol.prefix_levels(w)
@@ -468,6 +471,9 @@ def run_resnet(args):
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    from paper_2309_04875_b200 import _dev as _hb_dev
+
+    _hb_dev.bind_thread()  # the library's own CUDA runtime on this rank's device
     if args.workload == "resnet18":
         model, batch, shape = models.resnet18_cifar(0), args.batch or 512, (3, 32, 32)
     else:
@@ -571,6 +577,9 @@ def run_multi(args):
     local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    from paper_2309_04875_b200 import _dev as _hb_dev
+
+    _hb_dev.bind_thread()  # the library's own CUDA runtime on this rank's device
     if args.backend == "nccl":
         dist.init_process_group("nccl", device_id=dev)
     else:

@@ -90,6 +90,10 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
                       hb_triples_t arith0, hb_triples_t arith1, int drelu_only, int64_t chunk,
                       uint64_t* scratch, void* stream);
 
+/* Bind the calling host thread to CUDA device `device` (the library links its own CUDA runtime;
+ * the Python package calls this with torch's current device before any other entry point). */
+int hb_set_device(int device);
+
 /* ---- one party, staged: protocol.relu / protocol.drelu (protocol.py:179-199)
  * split at its exchanges.  Call round r = 0 .. hb_relu_rounds(): round r writes
  * this party's payload of round r into `own` (hb_relu_round_bytes bytes, except

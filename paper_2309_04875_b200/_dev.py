@@ -19,7 +19,16 @@ def device() -> torch.device:
         if not torch.cuda.is_available():
             raise RingMpcError("no CUDA device: this package runs its protocol only on the GPU")
         _DEVICE = torch.device("cuda", torch.cuda.current_device())
+        bind_thread()
     return _DEVICE
+
+
+def bind_thread() -> None:
+    """Point the library's own CUDA runtime at this thread's device (torch's current device): the
+    library links the runtime statically, so its per-thread current device is not torch's."""
+    from . import _lib
+
+    _lib.call("hb_set_device", torch.cuda.current_device())
 
 
 def is_device(a) -> bool:

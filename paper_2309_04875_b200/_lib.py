@@ -63,6 +63,7 @@ _SIGS = {
     "hb_relu_pair_host": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p, u64p,
                                          u64p, Triples, Triples, Triples, Triples, ctypes.c_int, ctypes.c_int64, u64p,
                                          ctypes.c_void_p]),
+    "hb_set_device": (ctypes.c_int, [ctypes.c_int]),
     "hb_relu_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "hb_relu_p2p_bytes": (ctypes.c_uint64, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_int64)]),

@@ -429,6 +429,12 @@ int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0,
                      "hb_relu_p2p_pair");
 }
 
+int hb_set_device(int device) {
+  // this library links its own (static) CUDA runtime: bind the calling thread to the caller's device
+  // explicitly instead of relying on the driver context another runtime made current
+  return cuda_status(cudaSetDevice(device), "hb_set_device");
+}
+
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr) {
   // a whole allocation of its own (CUDA IPC maps allocations, not sub-ranges of a caching
   // allocator's segment), zero-filled
