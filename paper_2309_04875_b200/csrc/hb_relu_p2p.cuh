@@ -89,13 +89,14 @@ struct P2PGeo {
   // the next round's inputs (helps the wide rounds only).  Measured on B200 with tools/micro/p2p_bench
   // (both parties on one GPU, 2^24; tools/micro_run2.sh / run4.sh): the kernel is latency-bound per
   // round, so more resident tiles win until registers spill -- w = 6: 6 CTAs (1.09e10 elem/s), w = 8:
-  // 5 (1.44e10; 6-8 are slower), w = 16 / 32: 7 (9.1e9 / 5.2e9, vs 8.5e9 / 4.3e9 at 5 / 4), w = 64: 4 +
-  // prefetch (0.97 of H).  Loading the next level's inputs into registers before each exchange
-  // (instead of after it) was slower at every width.
+  // 5 (1.44e10; 6-8 are slower), w = 16 / 32: 7 (9.1e9 / 5.2e9, vs 8.5e9 / 4.3e9 at 5 / 4), w = 64: 7 +
+  // prefetch (1.0 of H; 4 CTAs: 0.98).  With system-scope flags (two GPUs; tools/micro_run7.sh) more
+  // tiles in flight matter more: w = 64 0.52 -> 0.73 of H going from 4 to 7 CTAs.  Loading the next
+  // level's inputs into registers before each exchange (instead of after it) was slower at every width.
 #ifdef HB_P2P_MINB
   static constexpr int MINB = HB_P2P_MINB;
 #else
-  static constexpr int MINB = W == 8 ? 5 : (W < 8 ? 6 : (W <= 32 ? 7 : 4));
+  static constexpr int MINB = W == 8 ? 5 : (W < 8 ? 6 : 7);
 #endif
 #ifdef HB_P2P_PF
   static constexpr bool PF = HB_P2P_PF;

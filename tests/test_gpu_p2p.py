@@ -162,13 +162,17 @@ def test_p2p_parties_on_two_streams_layer_sequence():
     sizes = [_lib_bytes(n, km) for n, km in layers]
     links[0].ensure(max(b for b, _ in sizes), max(t for _, t in sizes))
     torch.cuda.synchronize()
+    # outputs allocated up front: an allocation between the two parties' launches can make the caching
+    # allocator synchronise the device (cudaFree), which would wait on the first party's spinning kernel
+    ybuf = [[torch.empty(n, dtype=torch.int64, device="cuda") for _ in (0, 1)] for n, _ in layers]
+    torch.cuda.synchronize()
     outs = []
     for i, (n, (k, m)) in enumerate(layers):
         ys = []
         for p in (0, 1):
             with torch.cuda.stream(st[p]):
                 ys.append(protocol.relu_p2p(sess[i][p], ArithShareTensor(p, 64, dev_in[i][p]), BitWindow(k, m),
-                                            links[p], stream=st[p]))
+                                            links[p], stream=st[p], out=ybuf[i][p]))
         outs.append(ys)
     for lk in links:
         lk.check(sync=True)
