@@ -52,8 +52,12 @@ def _scale(unit: str) -> float:
 
 
 def full(report: str, key: str, out: str = "profiles/ncu_summary.json") -> dict:
-    txt = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if report.endswith(".csv"):  # a `--page raw --csv` export made next to the capture
+        with open(report) as fh:
+            txt = fh.read()
+    else:
+        txt = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, val = rows[0], rows[1], rows[2]
     m = {}
