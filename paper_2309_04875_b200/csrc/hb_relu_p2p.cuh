@@ -44,7 +44,6 @@
 
 namespace hb {
 
-constexpr int P2P_TP = 128;  // threads per CTA
 
 // Memory-model scope of the flag protocol (P2PArgs::sys_scope, a uniform branch in the one thread
 // that handles the flags): system scope for parties on different GPUs (the peer is only in system
@@ -78,9 +77,19 @@ template <int W>
 struct P2PGeo {
   static constexpr int GS = Geo<W>::GS, PB = Geo<W>::PB, NB = PB / 8;
   static constexpr int L = constexpr_levels(W);
+  // threads per CTA (= per tile): one flag release per tile and round, so wide windows -- many
+  // bytes per element -- move more per release with 512-thread tiles (2 CTAs per SM); narrow ones
+  // keep 128 threads and more CTAs.  512 only while the byte-exact staging of 2 CTAs fits in shared
+  // memory.  Measured (tools/micro_run8.sh): w = 64: 1.0 -> 1.03 of H at gpu scope, 0.73 -> 0.82 at
+  // system scope; w = 32: 0.70 -> 0.73 / 0.49 -> 0.63; w = 8 / 16: no gain.
+#ifdef HB_P2P_TP
+  static constexpr int TP = HB_P2P_TP;
+#else
+  static constexpr int TP = (W >= 32 && 4 * P2P_C * 512 * NB <= 96 * 1024) ? 512 : 128;
+#endif
   static constexpr bool DIRECT = NB % 4 == 0;               // a group is whole 32-bit words
-  static constexpr u64 TE = (u64)P2P_C * P2P_TP * GS;       // elements per tile
-  static constexpr u64 SB = (u64)P2P_C * P2P_TP * NB;       // bytes of a bool segment per tile
+  static constexpr u64 TE = (u64)P2P_C * TP * GS;           // elements per tile
+  static constexpr u64 SB = (u64)P2P_C * TP * NB;           // bytes of a bool segment per tile
   static constexpr u64 SA = TE * 8;                         // bytes of an arith segment per tile
   static constexpr __host__ __device__ int nseg(int r) { return r == 0 ? 2 : (r <= L ? 4 : 2); }
   static constexpr __host__ __device__ u64 packet(int r) { return nseg(r) * (r <= L ? SB : SA); }
@@ -96,7 +105,7 @@ struct P2PGeo {
 #ifdef HB_P2P_MINB
   static constexpr int MINB = HB_P2P_MINB;
 #else
-  static constexpr int MINB = W == 8 ? 5 : (W < 8 ? 6 : 7);
+  static constexpr int MINB = TP == 512 ? 2 : (W == 8 ? 5 : (W < 8 ? 6 : 7));
 #endif
 #ifdef HB_P2P_PF
   static constexpr bool PF = HB_P2P_PF;
@@ -280,7 +289,7 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
   using G = Geo<W>;
   using K = Kit<W>;
   using PG = P2PGeo<W>;
-  constexpr int GS = G::GS, L = K::L, C = P2P_C, TP = P2P_TP, NB = PG::NB;
+  constexpr int GS = G::GS, L = K::L, C = P2P_C, TP = PG::TP, NB = PG::NB;
   constexpr u64 TE = PG::TE, SB = PG::SB, SA = PG::SA;
   const int t = threadIdx.x % TP;
   const bool p0 = A.party == 0;
@@ -548,7 +557,7 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
                                           uint8_t* __restrict__ stage) {
   constexpr u64 TE = P2PGeo<W>::TE;
   __shared__ int abort_s;
-  if (threadIdx.x % P2P_TP == 0) abort_s = 0;
+  if (threadIdx.x % P2PGeo<W>::TP == 0) abort_s = 0;
   // the FULL fast path loads / stores whole groups with 16-byte vectors: every per-element array
   // (x, y, the arith triple segments at the cursor and at +n) must be 16-byte aligned
   const PartyIO& io = A.io;
@@ -575,7 +584,7 @@ constexpr size_t p2p_smem_bytes() {
 // parties in one grid on one device (the single-GPU harness; the "remote" buffers are the other
 // party's): A1.grid > 0.
 template <int W>
-__global__ void __launch_bounds__(P2P_TP, P2PGeo<W>::MINB) k_relu_p2p(const P2PArgs A0, const P2PArgs A1) {
+__global__ void __launch_bounds__(P2PGeo<W>::TP, P2PGeo<W>::MINB) k_relu_p2p(const P2PArgs A0, const P2PArgs A1) {
   extern __shared__ __align__(16) uint8_t p2p_stage[];
   if (blockIdx.x < A0.grid)
     p2p_party<W>(A0, blockIdx.x, A0.grid, p2p_stage);
@@ -630,7 +639,7 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, int max_ctas1,
   // odd widths stage a bool round byte-exactly in shared memory: up to 126 KB at w = 63
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2P_TP, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2PGeo<W>::TP, smem);
   if (e != cudaSuccess) return e;
   // persistent cooperative grid: every CTA of the launch co-resident (the launch fails otherwise)
   const long long full = (long long)occ * sms;
@@ -652,7 +661,7 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, int max_ctas1,
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.gridDim = dim3((unsigned)(g0 + g1));
-  cfg.blockDim = dim3(P2P_TP);
+  cfg.blockDim = dim3(P2PGeo<W>::TP);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = attr;
