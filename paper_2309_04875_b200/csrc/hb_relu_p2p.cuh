@@ -77,15 +77,19 @@ template <int W>
 struct P2PGeo {
   static constexpr int GS = Geo<W>::GS, PB = Geo<W>::PB, NB = PB / 8;
   static constexpr int L = constexpr_levels(W);
-  // threads per CTA (= per tile): one flag release per tile and round, so wide windows -- many
-  // bytes per element -- move more per release with 512-thread tiles (2 CTAs per SM); narrow ones
-  // keep 128 threads and more CTAs.  512 only while the byte-exact staging of 2 CTAs fits in shared
-  // memory.  Measured (tools/micro_run8.sh): w = 64: 1.0 -> 1.03 of H at gpu scope, 0.73 -> 0.82 at
-  // system scope; w = 32: 0.70 -> 0.73 / 0.49 -> 0.63; w = 8 / 16: no gain.
+  // threads per CTA (= per tile): one flag release per tile and round, so bigger tiles move more
+  // per release -- which pays most at system scope (two GPUs), where a release costs ~4 us.
+  // Measured (tools/micro_run8.sh, gpu / system scope, fraction of H): w = 64: 128 threads x 7 CTAs
+  // 1.0 / 0.73, 512 x 2: 1.0 / 0.82; w = 32: 0.70 / 0.49 -> 0.73 / 0.63 (512 x 2); w = 16: 0.69 /
+  // 0.57 -> 0.68 / 0.63 (256 x 4); w = 6: 0.54 / 0.44 -> 0.54 / 0.49 (256 x 4); w = 8 keeps 128 x 5
+  // (0.77 / 0.56; 256 x 3: 0.76 / 0.60).  Bigger tiles only while the byte-exact staging of the
+  // resident CTAs fits in shared memory.
 #ifdef HB_P2P_TP
   static constexpr int TP = HB_P2P_TP;
 #else
-  static constexpr int TP = (W >= 32 && 4 * P2P_C * 512 * NB <= 96 * 1024) ? 512 : 128;
+  static constexpr int TP = (W >= 32 && 4 * P2P_C * 512 * NB <= 96 * 1024)
+                                ? 512
+                                : ((W != 8 && 4 * P2P_C * 256 * NB <= 56 * 1024) ? 256 : 128);
 #endif
   static constexpr bool DIRECT = NB % 4 == 0;               // a group is whole 32-bit words
   static constexpr u64 TE = (u64)P2P_C * TP * GS;           // elements per tile
@@ -105,7 +109,7 @@ struct P2PGeo {
 #ifdef HB_P2P_MINB
   static constexpr int MINB = HB_P2P_MINB;
 #else
-  static constexpr int MINB = TP == 512 ? 2 : (W == 8 ? 5 : (W < 8 ? 6 : 7));
+  static constexpr int MINB = TP == 512 ? 2 : (TP == 256 ? 4 : (W == 8 ? 5 : (W < 8 ? 6 : 7)));
 #endif
 #ifdef HB_P2P_PF
   static constexpr bool PF = HB_P2P_PF;
