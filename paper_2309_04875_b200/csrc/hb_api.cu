@@ -258,21 +258,17 @@ int hb_relu_pair_range(int ring_bits, int k, int m, int64_t n, int64_t first, in
 struct HostPipe {
   cudaStream_t in = nullptr, k = nullptr, out = nullptr;
   std::vector<cudaEvent_t> ev;
+  std::mutex busy;  // one pipelined call at a time per device (the events are reused)
 };
-static HostPipe& host_pipe(int dev, size_t nev) {
+static HostPipe& host_pipe(int dev) {
   static std::mutex mu;
   static std::map<int, HostPipe> pipes;
   std::lock_guard<std::mutex> g(mu);
-  HostPipe& p = pipes[dev];
+  HostPipe& p = pipes[dev];  // std::map: references stay valid as devices are added
   if (!p.in) {
     cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p.k, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&p.out, cudaStreamNonBlocking);
-  }
-  while (p.ev.size() < nev) {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    p.ev.push_back(e);
   }
   return p;
 }
@@ -312,7 +308,14 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  HostPipe& P = host_pipe(dev, 2 * ch.size() + 2);
+  HostPipe& P = host_pipe(dev);
+  std::lock_guard<std::mutex> hold(P.busy);
+  while (P.ev.size() < 2 * ch.size() + 2) {  // only the holder of `busy` touches the events
+    cudaEvent_t ev;
+    const cudaError_t ce = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (ce != cudaSuccess) return cuda_status(ce, "hb_relu_pair_host events");
+    P.ev.push_back(ev);
+  }
   uint64_t *d0 = scratch, *d1 = scratch + n, *e0 = scratch + 2 * n, *e1 = scratch + 3 * n;
   cudaEvent_t start = P.ev[2 * ch.size()], done = P.ev[2 * ch.size() + 1];
   // the scratch and the triples are ordered on the caller's stream
