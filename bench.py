@@ -835,7 +835,9 @@ def run_sweep(args):
             a = copy.copy(args)
             a.logn, a.k, a.m = logn, k, m
             a.no_e2e, a.no_cpu_baseline, a.no_resnet = True, True, True
-            a.graph = logn <= 22  # small layers: launch gaps would dominate the GPU time
+            # small layers: launch gaps would dominate the GPU time.  Not for the P2P path: its flags
+            # carry a host-advanced sequence, so a replayed graph would re-wait on satisfied flags
+            a.graph = logn <= 22 and args.path == "pair"
             a.steps = max(5, min(args.steps, 20))
             a.warmup = 3
             r = run_single(a)
@@ -844,8 +846,11 @@ def run_sweep(args):
                    "frac_vs_survey_H": r["roofline"]["frac_vs_survey_H"], "correct": r["correct"]}
             log(json.dumps(row))
             rows.append(row)
+            import gc
+
             import torch
 
+            gc.collect()  # the P2P links of a same-process pair reference each other (device buffers)
             torch.cuda.empty_cache()
     with open(args.sweep, "w") as fh:
         json.dump(rows, fh, indent=1)

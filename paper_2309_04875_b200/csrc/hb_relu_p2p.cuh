@@ -640,11 +640,19 @@ cudaError_t launch_p2p(P2PArgs A, const P2PArgs* B, int max_ctas, int max_ctas1,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = p2p_smem_bytes<W>();
   const void* fn = (const void*)k_relu_p2p<W>;
-  // odd widths stage a bool round byte-exactly in shared memory: up to 126 KB at w = 63
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2PGeo<W>::TP, smem);
-  if (e != cudaSuccess) return e;
+  // once per width and device: the shared-memory limit (odd widths stage a bool round byte-exactly:
+  // up to 126 KB at w = 63) and the co-resident CTAs per SM -- a per-launch query costs more host
+  // time than a small layer's kernel
+  static int occ_cache[16] = {};  // per device, 0 = not yet known
+  if (dev < 0 || dev >= 16 || occ_cache[dev] == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P2PGeo<W>::TP, smem);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 16) occ_cache[dev] = occ;
+  } else {
+    occ = occ_cache[dev];
+  }
   // persistent cooperative grid: every CTA of the launch co-resident (the launch fails otherwise)
   const long long full = (long long)occ * sms;
   auto clamp = [&](long long g, int mx) {
