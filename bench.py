@@ -343,7 +343,7 @@ def run_single(args):
         kernel = f"k_relu_p2p<{w}>"
         key = f"p2p_{args.p2p_scope}_w{w}_n{args.logn}"
     else:
-        kernel = f"k_relu_pair<{w}, 64, {1 if N == 64 else 0}>"
+        kernel = f"k_relu_pair<{w}, 32, {1 if N == 64 else 0}>"
         key = f"pair_w{w}_n{args.logn}"
     traffic = traffic_src = None
     try:

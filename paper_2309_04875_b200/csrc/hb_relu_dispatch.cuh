@@ -8,7 +8,7 @@
 namespace hb {
 
 #ifndef HB_PAIR_TP
-#define HB_PAIR_TP 64
+#define HB_PAIR_TP 32
 #endif
 constexpr int PAIR_TP = HB_PAIR_TP;  // threads per party per CTA (CTA = 2 * PAIR_TP)
 

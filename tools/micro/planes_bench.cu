@@ -30,7 +30,13 @@ HB_DEV void bytes_t4x(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32
   o[3] = __byte_perm(t2, t3, 0x7632);
 }
 
-constexpr int W = 8, TP = 64;
+#ifndef HB_MICRO_TP
+#define HB_MICRO_TP 64
+#endif
+#ifndef HB_MICRO_W
+#define HB_MICRO_W 8
+#endif
+constexpr int W = HB_MICRO_W, TP = HB_MICRO_TP;
 
 __global__ void k_fill(u64* p, u64 n, u64 seed) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
