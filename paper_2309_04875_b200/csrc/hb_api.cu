@@ -323,6 +323,12 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
   for (cudaStream_t st : {P.in, P.k, P.out})
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, start, 0);
   if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host");
+  // on a failure after work was queued, drain the internal streams before returning: the caller
+  // frees the scratch and host buffers the queued copies / kernels still reference
+  auto drain = [&](int rc) {
+    for (cudaStream_t st : {P.in, P.k, P.out}) (void)cudaStreamSynchronize(st);
+    return rc;
+  };
   for (size_t i = 0; i < ch.size(); ++i) {
     const int64_t lo = ch[i].first, c = ch[i].second;
     cudaEvent_t copied = P.ev[2 * i], computed = P.ev[2 * i + 1];
@@ -330,15 +336,15 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
     if (e == cudaSuccess) e = cudaMemcpyAsync(d1 + lo, hx1 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
     if (e == cudaSuccess) e = cudaEventRecord(copied, P.in);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(P.k, copied, 0);
-    if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host H2D");
+    if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host H2D"));
     const int rc = hb_relu_pair_range(ring_bits, k, m, n, lo, c, d0, d1, e0, e1, bool0, bool1, arith0, arith1,
                                       drelu_only, P.k);
-    if (rc) return rc;
+    if (rc) return drain(rc);
     e = cudaEventRecord(computed, P.k);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(P.out, computed, 0);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hy0 + lo, e0 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hy1 + lo, e1 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
-    if (e != cudaSuccess) return cuda_status(e, "hb_relu_pair_host D2H");
+    if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host D2H"));
   }
   e = cudaEventRecord(done, P.out);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(S(stream), done, 0);
