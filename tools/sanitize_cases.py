@@ -92,6 +92,17 @@ def case_conv():
             print(f"  conv b={b} c={c} h={h} oc={oc} k={kk} s={stride} party {party}: "
                   f"{'bit-exact' if this else 'MISMATCH'}")
             ok &= this
+        if c % 64 == 0:  # both parties' convs of the layer in one launch (model_forward_pair's path)
+            x1 = np.frombuffer(rng.bytes(8 * b * c * h * h), dtype="<u8").copy().reshape(b, c, h, h)
+            lw = nn._weight(wt, bias, FixedPointConfig())
+            outs = nn._conv_pair_dev([torch.from_numpy(v.view(np.int64)).cuda() for v in (x, x1)], "nchw", layer, lw,
+                                     (0, 1), 16)
+            for party, v in enumerate((x, x1)):
+                want = ON.conv2d(v, party, c, oc, kk, kk, stride, pad, wt, bias)
+                this = np.array_equal(outs[party].cpu().numpy().view(np.uint64), want)
+                print(f"  paired conv b={b} c={c} h={h} oc={oc} k={kk} s={stride} party {party}: "
+                      f"{'bit-exact' if this else 'MISMATCH'}")
+                ok &= this
     return ok
 
 
