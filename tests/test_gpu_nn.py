@@ -267,3 +267,35 @@ def test_every_resnet_conv_pair_launch_bit_exact(model, batch, geom):
             exp = want[p] if res is None else want[p] + res[p].cpu().numpy().view(np.uint64)
             assert np.array_equal(got, exp), (geom, p, fused)
     nn._PLANES.clear()
+
+
+def test_resnet18_full_forward_bit_exact_vs_oracle():
+    """The whole ResNet18-CIFAR private inference (batch 1, the benchmark's per-group 8-bit windows,
+    fused residual adds, paired conv launches, every ReLU through the fused pair kernel) equals the
+    oracle's run_local_forward (the reference algorithm restated, with Residual) exactly -- logits
+    and both parties' meter traces."""
+    model = models.resnet18_cifar(0)
+    wins = [(17, 9), (18, 10), (18, 10), (19, 11), (20, 12)]  # configs/resnet18_windows_w8.json
+    cfg = nn.ReluConfig([BitWindow(*w) for w in wins])
+    x_f = np.random.default_rng(33).uniform(0, 1, (1, 3, 32, 32))
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    want, traces, _ = ON.run_local_forward(layers, model.input_shape, model.weights, wins, x_f, 29)
+    logits, meters, _, _ = nn.run_local_forward(model, cfg, x_f, 29, pair=True, layer_logs=False)
+    assert np.array_equal(logits, want)
+    for p in (0, 1):
+        assert [tuple(t) for t in meters[p].trace] == [tuple(t) for t in traces[p]]
+
+
+def test_resnet50_full_forward_bit_exact_vs_oracle():
+    """The whole ResNet50 (64x64, CIFAR stem) private inference at batch 1 with the benchmark's
+    per-group 8-bit windows equals the oracle's run_local_forward exactly (bottleneck blocks, 1x1
+    convs up to 2048 channels, the N_T = 128 two-pass kernel at K up to 4608)."""
+    model = models.resnet50(0)
+    wins = [(17, 9), (18, 10), (20, 12), (22, 14), (23, 15)]  # configs/resnet50_windows_w8.json
+    cfg = nn.ReluConfig([BitWindow(*w) for w in wins])
+    x_f = np.random.default_rng(34).uniform(0, 1, (1, 3, 64, 64))
+    layers = [nn._layer_to_json(L) for L in model.layers]
+    want, traces, _ = ON.run_local_forward(layers, model.input_shape, model.weights, wins, x_f, 31)
+    logits, meters, _, _ = nn.run_local_forward(model, cfg, x_f, 31, pair=True, layer_logs=False)
+    assert np.array_equal(logits, want)
+    assert [tuple(t) for t in meters[0].trace] == [tuple(t) for t in traces[0]]
