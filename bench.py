@@ -707,6 +707,7 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
         r = torch.empty_like(enc).random_(generator=g)
         share = enc + r if party == 0 else -r
         mines = [ArithShareTensor(party, 64, share[i:i + mb]) for i in range(0, per_pair, mb)]
+        x_check = x_f[per_pair - mb:per_pair - mb + min(8, mb)].cpu().numpy()  # the last micro-batch's first images
         del x_f, enc, r
 
     def fwd():
@@ -736,9 +737,28 @@ def run_multi_resnet(args, dist, dev, rank, world, pairs, pair, party, active):
     ms = torch.tensor([a.elapsed_time(b)], device=dev if args.backend == "nccl" else "cpu")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
+    # fidelity (untimed): partners swap the logits shares of the last micro-batch's first images,
+    # party 0 reconstructs them and compares with the exact float forward of the same inputs
+    err = torch.zeros(1, device=ms.device)
+    if active:
+        last = fwd()
+        k8 = x_check.shape[0]
+        mine_l = last.data[:k8].reshape(-1).contiguous()
+        theirs = ep._swap(mine_l)
+        if not isinstance(theirs, torch.Tensor):
+            theirs = torch.from_numpy(np.frombuffer(theirs, dtype=np.int64).copy())
+        if party == 0:
+            from paper_2309_04875_b200 import simulator
+
+            rec = (mine_l.cpu() + theirs.cpu().reshape(-1)).numpy().astype(np.float64) / 65536.0
+            plain = simulator.plain_forward(model, x_check).reshape(-1)
+            err[0] = float(np.max(np.abs(rec - plain)))
+    dist.all_reduce(err, op=dist.ReduceOp.MAX)
     out = None
     if rank == 0:
         out = {
+            "logits_check": {"images_per_pair": int(x_check.shape[0]) if active else 0,
+                             "max_abs_diff_vs_plain_forward": float(err.item())},
             "metric": f"{args.workload}_private_inference_samples_per_s",
             "value": pairs * per_pair * args.steps / (total_ms / 1e3), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
