@@ -647,6 +647,39 @@ def run_multi(args):
         if party == 0:
             ok[0] = float(check_sample(mine_s[:c], theirs[:c], mine_s[c:], theirs[c:], N, k, m))
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    # e2e: the public per-party call with this rank's share in pinned host memory -- H2D of the share,
+    # the ReLU, D2H of the output share inside the timed region -- max over ranks
+    e2e = None
+    if not args.no_e2e:
+        h_in = mine.cpu().pin_memory() if active else None
+        h_out = torch.empty(n, dtype=torch.int64, pin_memory=True) if active else None
+        reps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            xd = h_in.to(dev, non_blocking=True)
+            yv = step_on(xd)
+            h_out.copy_(yv.data.reshape(-1), non_blocking=True)
+
+        def step_on(xd):
+            if store.remaining(dealer.BOOL, w) < need_b:
+                store.rewind(dealer.BOOL, w)
+                store.rewind(dealer.ARITH, N)
+            return protocol.relu(sess, ArithShareTensor(party, N, xd), win)
+
+        if active:
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        if active:
+            for _ in range(reps):
+                e2e_step()
+        torch.cuda.synchronize()
+        el = torch.tensor([time.perf_counter() - t0], device=ms.device)
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs * n * reps / float(el.item()), "unit": UNIT, "h2d_bytes_per_step": world * 8 * n,
+               "d2h_bytes_per_step": world * 8 * n, "steps": reps,
+               "path": "protocol.relu per party rank with its share in pinned host memory in and out (max over ranks)"}
     out = None
     if rank == 0:
         value = pairs * n * args.steps / (total_ms / 1e3)
@@ -662,7 +695,7 @@ def run_multi(args):
                        "parallelism": f"{pairs} party pairs"},
             "gpu_launches": args.steps * (1 if used_p2p else L + 4), "clocks": clk.summary(),
             "correct": bool(ok.item() > 0.5),
-            "e2e": None,
+            "e2e": e2e,
         }
     dist.destroy_process_group()
     return out
