@@ -329,19 +329,30 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
     for (cudaStream_t st : {P.in, P.k, P.out}) (void)cudaStreamSynchronize(st);
     return rc;
   };
+  // Three issue phases -- every H2D chunk, then every kernel range, then every D2H chunk -- so no
+  // D2H that waits on an event is queued between two H2D copies (with torch-level streams the
+  // interleaved order measured 7.9 ms per 2^24 step vs 6.3-6.5 ordered; natively both orders land
+  // at 6.2-7.0 ms, box to box -- tools/diag_zerocopy.py, tools/gpu_e2e_chunk_sweep.sh)
   for (size_t i = 0; i < ch.size(); ++i) {
     const int64_t lo = ch[i].first, c = ch[i].second;
-    cudaEvent_t copied = P.ev[2 * i], computed = P.ev[2 * i + 1];
     e = cudaMemcpyAsync(d0 + lo, hx0 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d1 + lo, hx1 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
-    if (e == cudaSuccess) e = cudaEventRecord(copied, P.in);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(P.k, copied, 0);
+    if (e == cudaSuccess) e = cudaEventRecord(P.ev[2 * i], P.in);
     if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host H2D"));
+  }
+  for (size_t i = 0; i < ch.size(); ++i) {
+    const int64_t lo = ch[i].first, c = ch[i].second;
+    e = cudaStreamWaitEvent(P.k, P.ev[2 * i], 0);
+    if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host"));
     const int rc = hb_relu_pair_range(ring_bits, k, m, n, lo, c, d0, d1, e0, e1, bool0, bool1, arith0, arith1,
                                       drelu_only, P.k);
     if (rc) return drain(rc);
-    e = cudaEventRecord(computed, P.k);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(P.out, computed, 0);
+    e = cudaEventRecord(P.ev[2 * i + 1], P.k);
+    if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host"));
+  }
+  for (size_t i = 0; i < ch.size(); ++i) {
+    const int64_t lo = ch[i].first, c = ch[i].second;
+    e = cudaStreamWaitEvent(P.out, P.ev[2 * i + 1], 0);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hy0 + lo, e0 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
     if (e == cudaSuccess) e = cudaMemcpyAsync(hy1 + lo, e1 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
     if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host D2H"));
