@@ -395,7 +395,8 @@ def run_single(args):
         r = run_resnet(ra)
         resnet = {"metric": r["metric"], "value": r["value"], "unit": r["unit"], "ms_per_step": r["ms_per_step"],
                   "config": r["config"], "steps": r["steps"], "warmup": r["warmup"],
-                  "logits_check": r["logits_check"], "cpu_estimate": rn_est}
+                  "logits_check": r["logits_check"], "cpu_estimate": rn_est,
+                  "layer_breakdown": r["layer_breakdown"]}
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -547,6 +548,27 @@ def run_resnet(args):
     logits_check = {"images": k8, "max_abs_diff_vs_plain_forward": float(np.max(np.abs(rec - plain))),
                     "argmax_agree": int(np.sum(np.argmax(rec, 1) == np.argmax(plain, 1))),
                     "plain_logit_absmax": float(np.max(np.abs(plain)))}
+    # per-layer device time of one (untimed, un-captured) micro-batch forward from CUDA events
+    # (nn.model_forward_pair(layer_times=...)), summed by layer kind; a residual block's own time is
+    # its fused last conv (+ the residual add) -- its entry minus its direct children's
+    for _ in range(2):  # the first eager pass populates the caching allocator outside the graph's pool
+        times = []
+        for st in stores:
+            for (kind, width) in need:
+                st.rewind(kind, width)
+        nn.model_forward_pair(sessions, x0s[0], x1s[0], model, cfg, layer_times=times)
+    by_kind = {}
+    for t in times:
+        ms_self = t["ms"]
+        if t["kind"] == "residual":
+            depth = t["layer"].count(".")
+            ms_self -= sum(u["ms"] for u in times if u["layer"].startswith(t["layer"] + ".")
+                           and u["layer"].count(".") == depth + 2)
+        key = "conv2d" if t["kind"] == "residual" else t["kind"]
+        by_kind[key] = by_kind.get(key, 0.0) + ms_self
+    layer_breakdown = {"micro_batch": mb, "ms_by_kind": {k: round(v, 3) for k, v in by_kind.items()},
+                       "note": "second eager forward (no CUDA graph), CUDA events per layer (host launch gaps "
+                               "included); conv2d includes the limb-plane split and the fused residual add"}
     return {
         "metric": f"{args.workload}_private_inference_samples_per_s", "value": batch / (ms / 1e3),
         "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -560,6 +582,7 @@ def run_resnet(args):
                            + ("hand-written tcgen05 kernel" if nn.RING_GEMM == "tc" else "cuBLASLt") + ") + fused pair ReLU kernel",
                    "weights": "random init (torchvision scheme), BN folded", "parallelism": "pair"},
         "relu_elems_per_s_in_model": relu_elems / (ms / 1e3), "logits_check": logits_check, "clocks": clk.summary(),
+        "layer_breakdown": layer_breakdown,
     }
 
 

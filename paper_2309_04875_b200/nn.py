@@ -586,19 +586,30 @@ def _meter_delta(ep, before):
     return sum(after[t][0] - before[t][0] for t in after), sum(after[t][1] - before[t][1] for t in after)
 
 
-def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_meter):
+def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_meter, layer_times=None):
     """Run the layers for one party (model_forward) or both parties on this GPU
     (model_forward_pair).  Shares stay on the device between layers, in NCHW: the
     ReLU consumes triples in element order, so keeping the reference's element order
-    is what makes the per-party shares (and the truncation after them) bit-exact."""
+    is what makes the per-party shares (and the truncation after them) bit-exact.
+
+    layer_times (a list, optional): every layer's device time, from CUDA events recorded on the
+    current stream around its launches -- {"layer", "kind", "ms"} per layer at every nesting level
+    (a Residual's entry includes its body's and shortcut's).  The per-round analogue of the
+    reference's wall_ms (cli.py:172-178) for the fused path, whose rounds run inside one kernel.
+    Not usable under CUDA-graph capture."""
     if len(relu_cfg.windows) != model.n_groups:
         raise ConfigError(f"relu config has {len(relu_cfg.windows)} groups, model needs {model.n_groups}")
     cfg = model.fixed_point
     parties = [s.party for s in sessions]
 
+    pending = []
+
     def run(layers, ds, lay, prefix):
         for i, L in enumerate(layers):
             before = [s.endpoint.meter.snapshot() for s in sessions]
+            if layer_times is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
             if isinstance(L, Relu):
                 win = relu_cfg.window_for(L.group_id)
                 if win is not None:
@@ -657,13 +668,21 @@ def _run_model(sessions, datas, model: ModelSpec, relu_cfg: ReluConfig, layer_me
                 for p, (s, bef) in enumerate(zip(sessions, before)):
                     nb, nr = _meter_delta(s.endpoint, bef)
                     layer_meter[p].append({"layer": f"{prefix}{i}:{L.kind}", "bytes": nb, "rounds": nr})
+            if layer_times is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record()
+                pending.append((f"{prefix}{i}", L.kind, ev0, ev1))
         return ds, lay
 
     try:
         ds, lay = run(model.layers, datas, "nchw" if datas[0].dim() == 4 else "flat", "")
     finally:
         _PLANES.clear()  # the limb-plane cache only serves convs sharing an input within one forward
-    return [_to_layout(d, lay, "nchw") for d in ds]
+    out = [_to_layout(d, lay, "nchw") for d in ds]
+    if layer_times is not None:
+        torch.cuda.synchronize()
+        layer_times.extend({"layer": name, "kind": kind, "ms": a.elapsed_time(b)} for name, kind, a, b in pending)
+    return out
 
 
 def model_forward(session: ProtocolSession, x: ArithShareTensor, model: ModelSpec, relu_cfg: ReluConfig,
@@ -675,11 +694,12 @@ def model_forward(session: ProtocolSession, x: ArithShareTensor, model: ModelSpe
 
 
 def model_forward_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, model: ModelSpec,
-                       relu_cfg: ReluConfig, layer_meter: tuple | None = None):
+                       relu_cfg: ReluConfig, layer_meter: tuple | None = None, layer_times: list | None = None):
     """Both parties on this GPU: local layers per party, every ReLU through the fused
-    pair kernel (protocol.relu_pair).  Same shares and meters as two model_forward threads."""
+    pair kernel (protocol.relu_pair).  Same shares and meters as two model_forward threads.
+    layer_times: see _run_model (per-layer device time from CUDA events)."""
     o0, o1 = _run_model(list(sessions), [_dev.to_device(x0.data), _dev.to_device(x1.data)], model, relu_cfg,
-                        layer_meter)
+                        layer_meter, layer_times)
     return (ArithShareTensor(0, x0.width, _dev.to_host(o0, x0.data)),
             ArithShareTensor(1, x1.width, _dev.to_host(o1, x1.data)))
 

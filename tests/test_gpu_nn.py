@@ -120,6 +120,33 @@ def test_wide_resnet_tma_fused_vs_oracle(pair):
     assert np.array_equal(logits2, want) and len(logs2[0]) > 0
 
 
+def test_layer_times_leave_the_forward_unchanged():
+    """model_forward_pair(layer_times=...) records one CUDA-event device time per layer (every
+    nesting level) and returns the same shares as the untimed forward (fused residual path)."""
+    from paper_2309_04875_b200 import ring, sharing, transport
+    from paper_2309_04875_b200.protocol import ProtocolSession
+
+    model = _wide_resnet()
+    cfg = nn.ReluConfig([BitWindow(22, 14), BitWindow(64, 0), BitWindow(20, 6)])
+    x_f = np.random.default_rng(8).uniform(0, 1, (3, 3, 8, 8))
+    enc = ring.encode_array(x_f, model.fixed_point)
+    s0, s1 = sharing.share_arith(enc, 64, np.random.default_rng(2))
+    outs = []
+    for times in (None, []):
+        stores = nn.build_stores(model, cfg, 3, 5)
+        eps = transport.local_pair()
+        sess = (ProtocolSession(eps[0], stores[0], model.fixed_point),
+                ProtocolSession(eps[1], stores[1], model.fixed_point))
+        outs.append(nn.model_forward_pair(sess, s0, s1, model, cfg, layer_times=times))
+        if times is not None:
+            kinds = [t["kind"] for t in times]
+            assert "relu" in kinds and "residual" in kinds and all(t["ms"] >= 0 for t in times)
+            top = [t for t in times if "." not in t["layer"]]
+            assert len(top) == len(model.layers)
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(np.asarray(a.data), np.asarray(b.data))
+
+
 def test_resnet18_forward_smoke():
     """Full ResNet18-CIFAR at batch 2: runs, spends the analytic rounds, and the logits
     track the plaintext fixed-point forward (fidelity, not exactness: local truncation)."""
