@@ -5,6 +5,7 @@
 // short triple streams are TripleExhaustedError (dealer.py:152-163), and all of
 // it is decided before the first kernel or exchange so both parties fail alike.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
@@ -316,7 +317,45 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
     if (ce != cudaSuccess) return cuda_status(ce, "hb_relu_pair_host events");
     P.ev.push_back(ev);
   }
-  uint64_t *d0 = scratch, *d1 = scratch + n, *e0 = scratch + 2 * n, *e1 = scratch + 3 * n;
+  // Both parties' shares of a chunk move in ONE two-row copy when the host buffers allow it (each
+  // copy costs ~20 us of fixed overhead on these boxes, comparable to a 1 MB transfer): the device
+  // rows are laid out in the host buffers' address order so both row pitches are positive.
+  const bool in_fwd = hx0 < hx1, out_fwd = hy0 < hy1;
+  uint64_t *d0 = scratch + (in_fwd ? 0 : n), *d1 = scratch + (in_fwd ? n : 0);
+  uint64_t *e0 = scratch + (out_fwd ? 2 * n : 3 * n), *e1 = scratch + (out_fwd ? 3 * n : 2 * n);
+  const size_t pin = (size_t)(in_fwd ? (const char*)hx1 - (const char*)hx0 : (const char*)hx0 - (const char*)hx1);
+  const size_t pout = (size_t)(out_fwd ? (const char*)hy1 - (const char*)hy0 : (const char*)hy0 - (const char*)hy1);
+  static const bool no2d = getenv("HB_PIPE_2D") && getenv("HB_PIPE_2D")[0] == '0';
+  int max_pitch = 0;
+  cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, dev);
+  const bool pitch_ok = (size_t)8 * n <= (size_t)max_pitch;
+  // a two-row copy is only valid when both rows lie in ONE host allocation (e.g. a pinned [2, n]
+  // buffer); the runtime rejects it otherwise (cudaErrorInvalidValue, synchronous, not sticky) and
+  // that direction falls back to one copy per share
+  bool row_in = !no2d && pitch_ok && pin >= (size_t)8 * n && pin <= (size_t)max_pitch;
+  bool row_out = !no2d && pitch_ok && pout >= (size_t)8 * n && pout <= (size_t)max_pitch;
+  auto h2d = [&](int64_t lo, int64_t c) {
+    if (row_in) {
+      const cudaError_t r = cudaMemcpy2DAsync(in_fwd ? d0 + lo : d1 + lo, 8 * (size_t)n, in_fwd ? hx0 + lo : hx1 + lo,
+                                              pin, 8 * c, 2, cudaMemcpyHostToDevice, P.in);
+      if (r != cudaErrorInvalidValue) return r;
+      (void)cudaGetLastError();
+      row_in = false;
+    }
+    cudaError_t r = cudaMemcpyAsync(d0 + lo, hx0 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
+    return r == cudaSuccess ? cudaMemcpyAsync(d1 + lo, hx1 + lo, 8 * c, cudaMemcpyHostToDevice, P.in) : r;
+  };
+  auto d2h = [&](int64_t lo, int64_t c) {
+    if (row_out) {
+      const cudaError_t r = cudaMemcpy2DAsync(out_fwd ? hy0 + lo : hy1 + lo, pout, out_fwd ? e0 + lo : e1 + lo,
+                                              8 * (size_t)n, 8 * c, 2, cudaMemcpyDeviceToHost, P.out);
+      if (r != cudaErrorInvalidValue) return r;
+      (void)cudaGetLastError();
+      row_out = false;
+    }
+    cudaError_t r = cudaMemcpyAsync(hy0 + lo, e0 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
+    return r == cudaSuccess ? cudaMemcpyAsync(hy1 + lo, e1 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out) : r;
+  };
   cudaEvent_t start = P.ev[2 * ch.size()], done = P.ev[2 * ch.size() + 1];
   // the scratch and the triples are ordered on the caller's stream
   cudaError_t e = cudaEventRecord(start, S(stream));
@@ -335,8 +374,7 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
   // at 6.2-7.0 ms, box to box -- tools/diag_zerocopy.py, tools/gpu_e2e_chunk_sweep.sh)
   for (size_t i = 0; i < ch.size(); ++i) {
     const int64_t lo = ch[i].first, c = ch[i].second;
-    e = cudaMemcpyAsync(d0 + lo, hx0 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d1 + lo, hx1 + lo, 8 * c, cudaMemcpyHostToDevice, P.in);
+    e = h2d(lo, c);
     if (e == cudaSuccess) e = cudaEventRecord(P.ev[2 * i], P.in);
     if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host H2D"));
   }
@@ -353,8 +391,7 @@ int hb_relu_pair_host(int ring_bits, int k, int m, int64_t n, const uint64_t* hx
   for (size_t i = 0; i < ch.size(); ++i) {
     const int64_t lo = ch[i].first, c = ch[i].second;
     e = cudaStreamWaitEvent(P.out, P.ev[2 * i + 1], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hy0 + lo, e0 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hy1 + lo, e1 + lo, 8 * c, cudaMemcpyDeviceToHost, P.out);
+    if (e == cudaSuccess) e = d2h(lo, c);
     if (e != cudaSuccess) return drain(cuda_status(e, "hb_relu_pair_host D2H"));
   }
   e = cudaEventRecord(done, P.out);

@@ -366,7 +366,8 @@ def _relu_pair_pinned(N, window, n, x0, x1, views, drelu_only, chunk=None):
     kernel, same triples, same shares as the one-shot path."""
     dev = _dev.device()
     h0, h1 = x0.data.reshape(-1), x1.data.reshape(-1)
-    o0, o1 = torch.empty(n, dtype=torch.int64, pin_memory=True), torch.empty(n, dtype=torch.int64, pin_memory=True)
+    o = torch.empty((2, n), dtype=torch.int64, pin_memory=True)  # one allocation: one two-row D2H per chunk
+    o0, o1 = o[0], o[1]
     scratch = torch.empty(4 * n, dtype=torch.int64, device=dev)
     _lib.call("hb_relu_pair_host", N, window.k, window.m, n, h0.data_ptr(), h1.data_ptr(), o0.data_ptr(),
               o1.data_ptr(), views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),

@@ -330,11 +330,14 @@ def test_gpu_drelu_from_shares_and_sim_relu():
     assert np.array_equal(out != 0.0, (ref_keep == 1) & (xf != 0.0))
 
 
-@pytest.mark.parametrize("n,chunk", [((1 << 22) + 12345, 1 << 20), ((1 << 22) + 7, 1 << 19)])
-def test_relu_pair_pinned_host_pipeline(n, chunk, monkeypatch):
+@pytest.mark.parametrize("n,chunk,layout", [((1 << 22) + 12345, 1 << 20, "separate"), ((1 << 22) + 7, 1 << 19, "separate"),
+                                            ((1 << 22) + 99, 1 << 20, "one_buffer_reversed")])
+def test_relu_pair_pinned_host_pipeline(n, chunk, layout, monkeypatch):
     """relu_pair on PINNED HOST shares (> 2^22 elements) runs the native pipeline hb_relu_pair_host
-    -- H2D / kernel on element ranges / D2H over three streams, ramped chunks, a partial last chunk --
-    and returns host shares equal to the device path's on the same triples, with the same meters."""
+    -- H2D / kernel on element ranges / D2H over three streams, ramped chunks, a partial last chunk,
+    both shares of a chunk in one two-row copy (also with party 1's share BELOW party 0's in one
+    pinned buffer: the reversed row order) -- and returns host shares equal to the device path's on
+    the same triples, with the same meters."""
     from paper_2309_04875_b200 import dealer
 
     monkeypatch.setattr(protocol, "_PIPE_CHUNK", chunk)
@@ -350,7 +353,11 @@ def test_relu_pair_pinned_host_pipeline(n, chunk, monkeypatch):
         dealer.stock_on_device(stores, (0, 1), dealer.ARITH, 64, 2 * n, seed=4)
         sess = (protocol.ProtocolSession(eps[0], stores[0]), protocol.ProtocolSession(eps[1], stores[1]))
         ts = [torch.from_numpy(v.view(np.int64)) for v in x]
-        ts = [t.pin_memory() for t in ts] if pinned else [t.cuda() for t in ts]
+        if pinned and layout == "one_buffer_reversed":
+            buf = torch.cat([ts[1], ts[0]]).pin_memory()
+            ts = [buf[n:], buf[:n]]
+        else:
+            ts = [t.pin_memory() for t in ts] if pinned else [t.cuda() for t in ts]
         r0, r1 = protocol.relu_pair(sess, ArithShareTensor(0, 64, ts[0]), ArithShareTensor(1, 64, ts[1]), BitWindow(k, m))
         if pinned:
             assert not r0.data.is_cuda
