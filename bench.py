@@ -912,9 +912,9 @@ def run_sweep(args):
             a = copy.copy(args)
             a.logn, a.k, a.m = logn, k, m
             a.no_e2e, a.no_cpu_baseline, a.no_resnet = True, True, True
-            # small layers: launch gaps would dominate the GPU time.  Not for the P2P path: its flags
-            # carry a host-advanced sequence, so a replayed graph would re-wait on satisfied flags
-            a.graph = logn <= 22 and args.path == "pair"
+            # small layers: launch gaps would dominate the GPU time (the P2P path replays too: its flag
+            # sequence and receive-region parity live on the device, advanced by the kernel itself)
+            a.graph = logn <= 22 and args.path in ("pair", "p2p")
             a.steps = max(5, min(args.steps, 20))
             a.warmup = 3
             r = run_single(a)

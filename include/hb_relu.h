@@ -133,6 +133,22 @@ int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0,
                      void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1, uint64_t seq0, int max_ctas0,
                      int max_ctas1, int sys_scope, double timeout_s, int* err_dev, int drelu_only,
                      uint64_t* wire_bytes_dev, void* stream);
+/* The same two launches with the link state on the DEVICE (graph-capturable): state_dev = three
+ * zero-initialised uint64 per party [flag sequence, launches, CTAs done], recv / peer_recv = the base
+ * of the two receive regions of region_bytes each (256-byte multiple).  The kernel reads seq0 and the
+ * region parity from the state and the party's last CTA advances them, so the arguments do not change
+ * from call to call and a sequence of layers can be replayed as one CUDA graph.  Replaces the same
+ * reference interface as hb_relu_p2p (protocol.py:195-199 over Endpoint.exchange, transport.py:129-133). */
+int hb_relu_p2p_dev(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+                    hb_triples_t bool_w, hb_triples_t arith_n, void* recv, const uint64_t* my_flags, void* peer_recv,
+                    uint64_t* peer_flags, uint64_t* state_dev, uint64_t region_bytes, int max_ctas, double timeout_s,
+                    int* err_dev, int drelu_only, uint64_t* wire_bytes_dev, void* stream);
+int hb_relu_p2p_pair_dev(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
+                         uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0,
+                         hb_triples_t arith1, void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1,
+                         uint64_t* state0, uint64_t* state1, uint64_t region_bytes, int max_ctas0, int max_ctas1,
+                         int sys_scope, double timeout_s, int* err_dev, int drelu_only, uint64_t* wire_bytes_dev,
+                         void* stream);
 /* CUDA IPC for the receive buffers / flags of a party on another GPU (64-byte handles); the buffers
  * are whole allocations (hb_dev_alloc, zero-filled) so a handle maps exactly them. */
 int hb_dev_alloc(uint64_t bytes, void** dev_ptr);

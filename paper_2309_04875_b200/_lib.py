@@ -76,6 +76,15 @@ _SIGS = {
                                         u64p, Triples, Triples, Triples, Triples, ctypes.c_void_p, ctypes.c_void_p,
                                         u64p, u64p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_double, ctypes.c_void_p, ctypes.c_int, u64p, ctypes.c_void_p]),
+    "hb_relu_p2p_dev": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p,
+                                       u64p, Triples, Triples, ctypes.c_void_p, u64p, ctypes.c_void_p, u64p, u64p,
+                                       ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int,
+                                       u64p, ctypes.c_void_p]),
+    "hb_relu_p2p_pair_dev": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p,
+                                            u64p, u64p, Triples, Triples, Triples, Triples, ctypes.c_void_p,
+                                            ctypes.c_void_p, u64p, u64p, u64p, u64p, ctypes.c_uint64, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int,
+                                            u64p, ctypes.c_void_p]),
     "hb_dev_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "hb_dev_free": (ctypes.c_int, [ctypes.c_void_p]),
     "hb_ipc_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),

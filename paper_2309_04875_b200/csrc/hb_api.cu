@@ -453,6 +453,8 @@ int p2p_args(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* 
   A.err = err_dev;
   A.wire_bytes = reinterpret_cast<unsigned long long*>(wire_bytes);
   A.stamps = nullptr;
+  A.state = nullptr;
+  A.region_bytes = 0;
   return HB_OK;
 }
 }  // namespace
@@ -484,6 +486,44 @@ int hb_relu_p2p_pair(int ring_bits, int k, int m, int64_t n, const uint64_t* x0,
   if (rc || n == 0) return rc;
   return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A0, &A1, max_ctas0, max_ctas1, sys_scope, S(stream)),
                      "hb_relu_p2p_pair");
+}
+
+int hb_relu_p2p_dev(int party, int ring_bits, int k, int m, int64_t n, const uint64_t* x, uint64_t* y,
+                    hb_triples_t boolw, hb_triples_t arith, void* recv, const uint64_t* my_flags, void* peer_recv,
+                    uint64_t* peer_flags, uint64_t* state_dev, uint64_t region_bytes, int max_ctas, double timeout_s,
+                    int* err_dev, int drelu_only, uint64_t* wire_bytes_dev, void* stream) {
+  if (!state_dev || (region_bytes & 255)) return fail(HB_ERR_CONFIG, "device link state and a 256-byte region needed");
+  hb::P2PArgs A;
+  const int rc = p2p_args(party, ring_bits, k, m, n, x, y, boolw, arith, recv, my_flags, peer_recv, peer_flags, 0,
+                          timeout_s, err_dev, drelu_only, wire_bytes_dev, A);
+  if (rc || n == 0) return rc;
+  A.state = reinterpret_cast<unsigned long long*>(state_dev);
+  A.region_bytes = region_bytes;
+  return cuda_status(
+      HB_RANGE_CALL(hb_p2p_dispatch, k - m, A, (const hb::P2PArgs*)nullptr, max_ctas, 0, 0, S(stream)),
+      "hb_relu_p2p_dev");
+}
+
+int hb_relu_p2p_pair_dev(int ring_bits, int k, int m, int64_t n, const uint64_t* x0, const uint64_t* x1, uint64_t* y0,
+                         uint64_t* y1, hb_triples_t bool0, hb_triples_t bool1, hb_triples_t arith0,
+                         hb_triples_t arith1, void* recv0, void* recv1, uint64_t* flags0, uint64_t* flags1,
+                         uint64_t* state0, uint64_t* state1, uint64_t region_bytes, int max_ctas0, int max_ctas1,
+                         int sys_scope, double timeout_s, int* err_dev, int drelu_only, uint64_t* wire_bytes_dev,
+                         void* stream) {
+  if (!state0 || !state1 || (region_bytes & 255))
+    return fail(HB_ERR_CONFIG, "device link states and a 256-byte region needed");
+  hb::P2PArgs A0, A1;
+  int rc = p2p_args(0, ring_bits, k, m, n, x0, y0, bool0, arith0, recv0, flags0, recv1, flags1, 0, timeout_s, err_dev,
+                    drelu_only, wire_bytes_dev, A0);
+  if (rc) return rc;
+  rc = p2p_args(1, ring_bits, k, m, n, x1, y1, bool1, arith1, recv1, flags1, recv0, flags0, 0, timeout_s, err_dev,
+                drelu_only, wire_bytes_dev, A1);
+  if (rc || n == 0) return rc;
+  A0.state = reinterpret_cast<unsigned long long*>(state0);
+  A1.state = reinterpret_cast<unsigned long long*>(state1);
+  A0.region_bytes = A1.region_bytes = region_bytes;
+  return cuda_status(HB_RANGE_CALL(hb_p2p_dispatch, k - m, A0, &A1, max_ctas0, max_ctas1, sys_scope, S(stream)),
+                     "hb_relu_p2p_pair_dev");
 }
 
 int hb_set_device(int device) {

@@ -71,6 +71,12 @@ struct P2PArgs {
   int* err;                       // set to 1 on a spin timeout
   unsigned long long* wire_bytes; // optional [P2P_MAXR] counters of the bytes stored to the peer
   unsigned long long* stamps;     // optional phase timestamps (tools/micro/p2p_bench), else null
+  // Device-resident link state (optional, this party only): [0] flag sequence, [1] launches, [2]
+  // CTAs done.  When set, seq0 and the receive region (launch parity x region_bytes past recv /
+  // peer_recv) come from the device and the party's last CTA advances them -- the launch arguments
+  // are then the same every call, so a sequence of layers can be captured in a CUDA graph.
+  unsigned long long* state;
+  u64 region_bytes;
 };
 
 template <int W>
@@ -289,7 +295,8 @@ HB_DEV void st_grp(u64* p, int valid, const u64 (&v)[GS]) {
 // Returns false when the peer timed out.  `wbytes` accumulates the bytes stored to the peer.
 template <int W, bool FULL>
 __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, const u64 tile, const u64 it,
-                                         uint8_t* __restrict__ stage, int& abort_s, u64& wbytes) {
+                                         uint8_t* __restrict__ stage, int& abort_s, u64& wbytes, const u64 seq0,
+                                         const u64 roff) {
   using G = Geo<W>;
   using K = Kit<W>;
   using PG = P2PGeo<W>;
@@ -317,7 +324,7 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
 #ifdef HB_P2P_STAMPS
   if (A.stamps && t == 0 && cta < 4 && it < 32) stamp = A.stamps + ((A.party * 4 + cta) * 32 + it) * (P2P_MAXR * 5);
 #endif
-  auto pkt = [&](uint8_t* base, int r) -> uint8_t* { return base + A.round_off[r] + tile * PG::packet(r); };
+  auto pkt = [&](uint8_t* base, int r) -> uint8_t* { return base + roff + A.round_off[r] + tile * PG::packet(r); };
 
   // ---- bool openings: direct coalesced stores into the peer's packet, or byte-exact staging
   auto put_bool = [&](int r, int sg, int c, const Cg<W>& v) {
@@ -397,7 +404,7 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
     if (t == 0) {
       // the CTA's stores to the peer are ordered before this thread by the barrier; the release
       // store is cumulative over them at system scope
-      const unsigned long long seq = A.seq0 + (u64)r + 1;
+      const unsigned long long seq = seq0 + (u64)r + 1;
       flag_release(A.sys_scope, A.peer_flag + tile, seq);
       if (stamp) stamp[r * 5 + 2] = globaltimer();
       if (flag_relaxed(A.sys_scope, A.my_flag + tile) < seq) {
@@ -569,13 +576,33 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
                        reinterpret_cast<uintptr_t>(io.aa + io.acur) | reinterpret_cast<uintptr_t>(io.ab + io.acur) |
                        reinterpret_cast<uintptr_t>(io.ac + io.acur) | (uintptr_t)(8 * A.n);
   const bool aligned = Geo<W>::GS % 2 == 1 ? (al & 7) == 0 : (al & 15) == 0;
+  u64 seq0 = A.seq0, roff = 0;
+  if (A.state) {  // written by this party's previous launch (stream order), read by every CTA first
+    seq0 = __ldcg(A.state);
+    roff = (__ldcg(A.state + 1) & 1ull) * A.region_bytes;
+  }
   u64 wbytes = 0, it = 0;
   for (u64 tile = cta; tile < A.ntiles; tile += ncta, ++it) {
-    const bool ok = aligned && (tile + 1) * TE <= A.n ? p2p_tile<W, true>(A, cta, tile, it, stage, abort_s, wbytes)
-                                           : p2p_tile<W, false>(A, cta, tile, it, stage, abort_s, wbytes);
-    if (!ok) return;
+    const bool ok = aligned && (tile + 1) * TE <= A.n
+                        ? p2p_tile<W, true>(A, cta, tile, it, stage, abort_s, wbytes, seq0, roff)
+                        : p2p_tile<W, false>(A, cta, tile, it, stage, abort_s, wbytes, seq0, roff);
+    if (!ok) return;  // timed out: the error word is set and the link is dead (state left as is)
   }
   if (A.wire_bytes && wbytes) atomicAdd(A.wire_bytes, (unsigned long long)wbytes);
+  if (A.state) {
+    // the party's last CTA to finish (every CTA read the state before it got here) advances the
+    // sequence by this launch's rounds and flips the region parity for the next launch
+    __syncthreads();
+    if (threadIdx.x % P2PGeo<W>::TP == 0) {
+      __threadfence();
+      if (atomicAdd(A.state + 2, 1ull) == ncta - 1) {
+        A.state[0] = seq0 + (u64)(Kit<W>::L + (A.drelu_only ? 2 : 3));
+        A.state[1] += 1;
+        A.state[2] = 0;
+        __threadfence();
+      }
+    }
+  }
 }
 
 template <int W>

@@ -244,21 +244,17 @@ def relu_p2p_pair(sessions, x0: ArithShareTensor, x1: ArithShareTensor, window: 
     nbytes = lib.hb_relu_p2p_bytes(k, m, n, int(drelu_only), ctypes.byref(ntiles))
     l0.check()
     l0.ensure(nbytes, ntiles.value)
-    rounds = lib.hb_relu_rounds(k, m, int(drelu_only))
-    seq0 = l0.seq
-    l0.seq += rounds
-    l1.seq += rounds
-    r0, _ = l0.region()
-    r1, _ = l1.region()
     y0 = torch.empty(n, dtype=torch.int64, device=a0.device)
     y1 = torch.empty(n, dtype=torch.int64, device=a0.device)
     wc = l0.wire_counter
     cur = torch.cuda.current_stream()  # once: the query costs more host time than a small layer's kernel
-    _lib.check(lib.hb_relu_p2p_pair(N, k, m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
-                                    views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),
-                                    r0, r1, l0.flags, l1.flags, seq0, l0.max_ctas, l1.max_ctas, int(sys_scope),
-                                    l0.timeout_s, l0.err.data_ptr(), int(drelu_only),
-                                    None if wc is None else wc.data_ptr(), cur.cuda_stream))
+    # flag sequence and receive-region parity come from the links' device state (graph-capturable)
+    _lib.check(lib.hb_relu_p2p_pair_dev(N, k, m, n, a0.data_ptr(), a1.data_ptr(), y0.data_ptr(), y1.data_ptr(),
+                                        views[0][0].abi(), views[1][0].abi(), views[0][1].abi(), views[1][1].abi(),
+                                        l0.recv, l1.recv, l0.flags, l1.flags, l0.state.data_ptr(),
+                                        l1.state.data_ptr(), l0.cap_bytes, l0.max_ctas, l1.max_ctas, int(sys_scope),
+                                        l0.timeout_s, l0.err.data_ptr(), int(drelu_only),
+                                        None if wc is None else wc.data_ptr(), cur.cuda_stream))
     l0.after_launch(cur)
     return (_wrap(ArithShareTensor, 0, N, y0, x0.data, x0.shape), _wrap(ArithShareTensor, 1, N, y1, x1.data, x1.shape))
 
@@ -286,10 +282,6 @@ def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, l
     nbytes = lib.hb_relu_p2p_bytes(k, m, n, int(drelu_only), ctypes.byref(ntiles))
     link.check()
     link.ensure(nbytes, ntiles.value)
-    rounds = lib.hb_relu_rounds(k, m, int(drelu_only))
-    seq0 = link.seq
-    link.seq += rounds
-    own, peer = link.region()
     session.endpoint.meter.record_rounds(_relu_trace(n, k, m, N, bool(drelu_only)))
     y = torch.empty(n, dtype=torch.int64, device=xd.device) if out is None else out.reshape(-1)
     if y.numel() != n or y.dtype != torch.int64 or not y.is_cuda:
@@ -297,9 +289,11 @@ def relu_p2p(session: ProtocolSession, x: ArithShareTensor, window: BitWindow, l
     launch_stream = torch.cuda.current_stream() if stream is None else stream
     st = launch_stream.cuda_stream
     wc = link.wire_counter
-    _lib.check(lib.hb_relu_p2p(session.party, N, k, m, n, xd.data_ptr(), y.data_ptr(), bv.abi(), av.abi(),
-                               own, link.flags, peer, link.peer_flags, seq0, link.grid, link.timeout_s,
-                               link.err.data_ptr(), int(drelu_only), None if wc is None else wc.data_ptr(), st))
+    # flag sequence and receive-region parity from the link's device state (graph-capturable)
+    _lib.check(lib.hb_relu_p2p_dev(session.party, N, k, m, n, xd.data_ptr(), y.data_ptr(), bv.abi(), av.abi(),
+                                   link.recv, link.flags, link.peer_recv, link.peer_flags, link.state.data_ptr(),
+                                   link.cap_bytes, link.grid, link.timeout_s, link.err.data_ptr(), int(drelu_only),
+                                   None if wc is None else wc.data_ptr(), st))
     link.after_launch(launch_stream)
     return _wrap(ArithShareTensor, x.party, N, y, x.data, x.shape)
 

@@ -255,3 +255,45 @@ def test_p2p_two_processes_ipc(tmp_path):
     q0, q1 = protocol.relu_pair((s0, s1), ArithShareTensor(0, 64, x0), ArithShareTensor(1, 64, x1), BitWindow(22, 14))
     assert np.array_equal(y0.view(np.uint64), np.asarray(q0.data).view(np.uint64))
     assert np.array_equal(y1.view(np.uint64), np.asarray(q1.data).view(np.uint64))
+
+
+def test_p2p_layers_replayed_as_cuda_graph():
+    """A sequence of layers through the NVLink party kernels captured in ONE CUDA graph and replayed
+    twice: the flag sequence and the receive-region parity live on the device (PeerLink.state, the
+    kernel's last CTA advances them), so the launch arguments never change and every replay is a
+    fresh, correctly sequenced run -- shares equal the eager launches' on the same triples."""
+    links = transport.local_p2p_pair()
+    links[0].timeout_s = 20.0
+    layers = [((1 << 16) + 5, (22, 14)), ((1 << 18), (64, 0)), (40000, (20, 6))]
+    sess, ins = [], []
+    for i, (n, (k, m)) in enumerate(layers):
+        x0, x1 = gc.baseline_inputs(n, seed=50 + i)
+        s0, s1, _ = stocked_sessions_for_relu(n, k - m, 64, seed=60 + i)
+        sess.append((s0, s1))
+        ins.append((ArithShareTensor(0, 64, torch.from_numpy(x0.view(np.int64)).cuda()),
+                    ArithShareTensor(1, 64, torch.from_numpy(x1.view(np.int64)).cuda())))
+
+    def forward():
+        return [protocol.relu_p2p_pair(s, a, b, BitWindow(*km), links) for s, (a, b), (_, km) in zip(sess, ins, layers)]
+
+    def rewind():
+        for (s0, s1), (_, (k, m)) in zip(sess, layers):
+            for s in (s0, s1):
+                s.triples.rewind("bool", k - m)
+                s.triples.rewind("arith", 64)
+
+    want = [(a.data.clone(), b.data.clone()) for a, b in forward()]  # eager (also sizes the buffers)
+    links[0].check(sync=True)
+    launches0 = int(links[0].state[1])
+    rewind()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        outs = forward()
+    for _ in range(2):
+        g.replay()
+        links[0].check(sync=True)
+        for (a, b), (wa, wb) in zip(outs, want):
+            assert torch.equal(a.data, wa) and torch.equal(b.data, wb)
+    # every replayed launch advanced both parties' device sequences identically
+    assert torch.equal(links[0].state[:2], links[1].state[:2])
+    assert int(links[0].state[1]) == launches0 + 2 * len(layers)

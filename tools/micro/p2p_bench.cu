@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
   const u64 n = 1ull << logn;
   const int L = constexpr_levels(W), R = L + 3;
   const u64 nb = n * (1 + 2 * L), nbw = (nb * W + 63) / 64;
-  P2PArgs A[2];
+  P2PArgs A[2] = {};
   u64 off[P2P_MAXR], ntiles = 0;
   const u64 rbytes = p2p_layout<W>(n, 0, off, &ntiles);
   int* err;
