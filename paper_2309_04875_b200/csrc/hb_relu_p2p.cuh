@@ -76,7 +76,7 @@ struct P2PArgs {
   // peer_recv) come from the device and the party's last CTA advances them -- the launch arguments
   // are then the same every call, so a sequence of layers can be captured in a CUDA graph.
   unsigned long long* state;
-  u64 region_bytes;
+  u64 region_bytes;               // offset of the second receive region (odd launches)
 };
 
 template <int W>
@@ -290,13 +290,16 @@ HB_DEV void st_grp(u64* p, int valid, const u64 (&v)[GS]) {
   }
 }
 
+// Per-CTA launch constants of the party kernel: [0] flag sequence base (read by the flag thread
+// each round, so no register holds it across the tile), [1] receive-region offset.
+__shared__ u64 p2p_link_s[2];
+
 // One tile of one party: all rounds.  FULL = every element of the tile is in the layer (the
 // direct-store fast path); the partial last tile stages every bool round byte-exactly.
 // Returns false when the peer timed out.  `wbytes` accumulates the bytes stored to the peer.
 template <int W, bool FULL>
 __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, const u64 tile, const u64 it,
-                                         uint8_t* __restrict__ stage, int& abort_s, u64& wbytes, const u64 seq0,
-                                         const u64 roff) {
+                                         uint8_t* __restrict__ stage, int& abort_s, u64& wbytes, const u64 roff) {
   using G = Geo<W>;
   using K = Kit<W>;
   using PG = P2PGeo<W>;
@@ -324,13 +327,18 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
 #ifdef HB_P2P_STAMPS
   if (A.stamps && t == 0 && cta < 4 && it < 32) stamp = A.stamps + ((A.party * 4 + cta) * 32 + it) * (P2P_MAXR * 5);
 #endif
-  auto pkt = [&](uint8_t* base, int r) -> uint8_t* { return base + roff + A.round_off[r] + tile * PG::packet(r); };
+  // this launch's receive region: the kernel-parameter base plus the launch's region offset (0 or
+  // region_bytes by launch parity, from the device link state; read once per party)
+  auto pkt = [&](bool peer, int r) -> uint8_t* {
+    uint8_t* base = (peer ? A.peer_recv : A.recv) + roff;
+    return base + A.round_off[r] + tile * PG::packet(r);
+  };
 
   // ---- bool openings: direct coalesced stores into the peer's packet, or byte-exact staging
   auto put_bool = [&](int r, int sg, int c, const Cg<W>& v) {
     Pk<W> p = to_packed<W>(v);
     if constexpr (PG::DIRECT && full) {
-      put_peer<W>(pkt(A.peer_recv, r) + sg * SB + (u64)(c * TP + t) * NB, p);
+      put_peer<W>(pkt(true, r) + sg * SB + (u64)(c * TP + t) * NB, p);
       wbytes += NB;
     } else {
       pk_trim<W>(p, valid[c]);
@@ -343,7 +351,7 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
     __syncthreads();
     const unsigned vb = (unsigned)((cnt * W + 7) / 8);  // <= SB
     const unsigned ns = PG::nseg(r);
-    uint8_t* dst = pkt(A.peer_recv, r);
+    uint8_t* dst = pkt(true, r);
     const unsigned nv = vb / 16;
     for (unsigned sg = 0; sg < ns; ++sg)
       for (unsigned k = t; k < nv; k += TP)
@@ -354,16 +362,16 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
     if (t == 0) wbytes += (u64)vb * ns;
   };
   auto get_bool = [&](int r, int sg, int c) -> Cg<W> {
-    const u64* s = reinterpret_cast<const u64*>(pkt(A.recv, r) + sg * SB);
+    const u64* s = reinterpret_cast<const u64*>(pkt(false, r) + sg * SB);
     return from_packed<W>(load_pk_cg<W>(s, (u64)(c * TP + t) * GS, SB / 8));
   };
   auto put_arith = [&](int r, int sg, int c, const u64 (&v)[GS]) {
-    u64* d = reinterpret_cast<u64*>(pkt(A.peer_recv, r) + sg * SA) + (u64)(c * TP + t) * GS;
+    u64* d = reinterpret_cast<u64*>(pkt(true, r) + sg * SA) + (u64)(c * TP + t) * GS;
     st_grp<GS, FULL>(d, valid[c], v);
     wbytes += 8 * (u64)valid[c];
   };
   auto get_arith = [&](int r, int sg, int c, u64 (&v)[GS]) {
-    ld_grp_cg<GS, FULL>(reinterpret_cast<const u64*>(pkt(A.recv, r) + sg * SA) + (u64)(c * TP + t) * GS, valid[c], v);
+    ld_grp_cg<GS, FULL>(reinterpret_cast<const u64*>(pkt(false, r) + sg * SA) + (u64)(c * TP + t) * GS, valid[c], v);
   };
   auto bseg = [&](const u64* arr, int sgi, int c) { return load_cg<W>(arr, io.bcur + (u64)sgi * n + e0[c], io.bnw); };
 
@@ -404,7 +412,7 @@ __device__ __forceinline__ bool p2p_tile(const P2PArgs& A, const unsigned cta, c
     if (t == 0) {
       // the CTA's stores to the peer are ordered before this thread by the barrier; the release
       // store is cumulative over them at system scope
-      const unsigned long long seq = seq0 + (u64)r + 1;
+      const unsigned long long seq = *reinterpret_cast<volatile u64*>(&p2p_link_s[0]) + (u64)r + 1;
       flag_release(A.sys_scope, A.peer_flag + tile, seq);
       if (stamp) stamp[r * 5 + 2] = globaltimer();
       if (flag_relaxed(A.sys_scope, A.my_flag + tile) < seq) {
@@ -576,16 +584,19 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
                        reinterpret_cast<uintptr_t>(io.aa + io.acur) | reinterpret_cast<uintptr_t>(io.ab + io.acur) |
                        reinterpret_cast<uintptr_t>(io.ac + io.acur) | (uintptr_t)(8 * A.n);
   const bool aligned = Geo<W>::GS % 2 == 1 ? (al & 7) == 0 : (al & 15) == 0;
-  u64 seq0 = A.seq0, roff = 0;
-  if (A.state) {  // written by this party's previous launch (stream order), read by every CTA first
-    seq0 = __ldcg(A.state);
-    roff = (__ldcg(A.state + 1) & 1ull) * A.region_bytes;
+  if (threadIdx.x % P2PGeo<W>::TP == 0) {
+    // this launch's flag sequence base and receive-region offset: the host's, or the device link
+    // state written by this party's previous launch (stream order)
+    p2p_link_s[0] = A.state ? __ldcg(A.state) : A.seq0;
+    p2p_link_s[1] = A.state ? (__ldcg(A.state + 1) & 1ull) * A.region_bytes : 0ull;
   }
+  __syncthreads();
+  const u64 roff = p2p_link_s[1];
   u64 wbytes = 0, it = 0;
   for (u64 tile = cta; tile < A.ntiles; tile += ncta, ++it) {
     const bool ok = aligned && (tile + 1) * TE <= A.n
-                        ? p2p_tile<W, true>(A, cta, tile, it, stage, abort_s, wbytes, seq0, roff)
-                        : p2p_tile<W, false>(A, cta, tile, it, stage, abort_s, wbytes, seq0, roff);
+                        ? p2p_tile<W, true>(A, cta, tile, it, stage, abort_s, wbytes, roff)
+                        : p2p_tile<W, false>(A, cta, tile, it, stage, abort_s, wbytes, roff);
     if (!ok) return;  // timed out: the error word is set and the link is dead (state left as is)
   }
   if (A.wire_bytes && wbytes) atomicAdd(A.wire_bytes, (unsigned long long)wbytes);
@@ -596,7 +607,7 @@ __device__ __forceinline__ void p2p_party(const P2PArgs& A, const unsigned cta, 
     if (threadIdx.x % P2PGeo<W>::TP == 0) {
       __threadfence();
       if (atomicAdd(A.state + 2, 1ull) == ncta - 1) {
-        A.state[0] = seq0 + (u64)(Kit<W>::L + (A.drelu_only ? 2 : 3));
+        A.state[0] = p2p_link_s[0] + (u64)(Kit<W>::L + (A.drelu_only ? 2 : 3));
         A.state[1] += 1;
         A.state[2] = 0;
         __threadfence();
