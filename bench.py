@@ -645,12 +645,26 @@ def run_multi(args):
             y = step()
     torch.cuda.synchronize()
     dist.barrier()
+    graph = None
+    if args.graph and used_p2p:
+        # each party rank's timed steps as ONE CUDA graph: the party kernel's flag sequence and receive
+        # region live on the device (PeerLink.state), so the replays of the two ranks stay in step
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(args.steps):
+                y = step()
+        graph.replay()  # warm (the partner rank replays too)
+        torch.cuda.synchronize()
+        ep.p2p.check(sync=True)
+        dist.barrier()
     with ClockSampler(local) as clk:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         dist.barrier()
         a.record(s)
-        if active:
+        if graph is not None:
+            graph.replay()
+        elif active:
             for _ in range(args.steps):
                 y = step()
         b.record(s)
@@ -716,7 +730,7 @@ def run_multi(args):
                        "path": ("one-launch NVLink party kernel hb_relu_p2p, openings stored into the peer's "
                                 "buffer (CUDA IPC) with per-chunk flags (ranks 2i<->2i+1)") if used_p2p
                        else f"staged hb_relu_round + {args.backend} send/recv per round (ranks 2i<->2i+1)",
-                       "parallelism": f"{pairs} party pairs"},
+                       "cuda_graph": graph is not None, "parallelism": f"{pairs} party pairs"},
             "gpu_launches": args.steps * (1 if used_p2p else L + 4), "clocks": clk.summary(),
             "correct": bool(ok.item() > 0.5),
             "e2e": e2e,
