@@ -176,6 +176,10 @@ def test_p2p_parties_on_two_streams_layer_sequence():
         outs.append(ys)
     for lk in links:
         lk.check(sync=True)
+    # each party's kernels advanced its own device link state by every launch's rounds
+    want_seq = sum(protocol.prefix_levels(k - m) + 3 for _, (k, m) in layers)
+    for lk in links:
+        assert lk.state.tolist() == [want_seq, len(layers), 0]
     for i, (n, (k, m)) in enumerate(layers):
         q0, q1 = stocked_sessions_for_relu(n, k - m, 64, seed=40 + i)[:2]
         w0, w1 = protocol.relu_pair((q0, q1), ArithShareTensor(0, 64, dev_in[i][0]), ArithShareTensor(1, 64, dev_in[i][1]),
@@ -284,7 +288,7 @@ def test_p2p_layers_replayed_as_cuda_graph():
 
     want = [(a.data.clone(), b.data.clone()) for a, b in forward()]  # eager (also sizes the buffers)
     links[0].check(sync=True)
-    launches0 = int(links[0].state[1])
+    launches0, seq0 = int(links[0].state[1]), int(links[0].state[0])
     rewind()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
@@ -294,6 +298,10 @@ def test_p2p_layers_replayed_as_cuda_graph():
         links[0].check(sync=True)
         for (a, b), (wa, wb) in zip(outs, want):
             assert torch.equal(a.data, wa) and torch.equal(b.data, wb)
-    # every replayed launch advanced both parties' device sequences identically
+    # every replayed launch advanced both parties' device sequences identically, by its rounds, and
+    # the last CTA reset the done counter
     assert torch.equal(links[0].state[:2], links[1].state[:2])
     assert int(links[0].state[1]) == launches0 + 2 * len(layers)
+    assert int(links[0].state[2]) == 0 and int(links[1].state[2]) == 0
+    seq_per_pass = sum(protocol.prefix_levels(k - m) + 3 for _, (k, m) in layers)
+    assert int(links[0].state[0]) == seq0 + 2 * seq_per_pass
