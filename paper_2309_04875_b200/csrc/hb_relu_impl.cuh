@@ -123,9 +123,20 @@ struct PairGeo {
   static constexpr int SEGW = (4 * PW > 2 * GS) ? 4 * PW : 2 * GS;  // words per thread per wire buffer
 };
 
-#ifndef HB_PAIR_MINB
-#define HB_PAIR_MINB 1
+// Resident CTAs per SM the pair kernel's register budget is set for (__launch_bounds__ min blocks).
+// The kernel issues every load of a group up front, so more resident warps = more bytes in flight:
+// widths 2/4/6/8 compile to 96-112 registers unconstrained (8 CTAs of 64 threads per SM) and fit 96
+// without spills -> 10 CTAs per SM: w = 8 at 2^24 3.59e10 -> 4.03e10 elements/s (same-box A/B,
+// tools/gpu_ab_lib.sh); forcing 12 (80 registers) spills and is slower (3.39e10).  Odd and wider
+// widths need more registers and keep the compiler's choice.  HB_PAIR_MINB overrides (experiments).
+template <int W>
+constexpr int pair_minb() {
+#ifdef HB_PAIR_MINB
+  return HB_PAIR_MINB;
+#else
+  return (W <= 8 && W % 2 == 0) ? 10 : 1;
 #endif
+}
 // One group of both parties' elements through every round: thread t of party `party` owns the GS
 // elements starting at layer element e0 (`valid` of them in the layer); the peer thread (t of the
 // other half of the CTA) owns the same elements.  Returns the output share (or the DReLU share when
@@ -261,7 +272,7 @@ HB_DEV void pair_group(const PairArgs& A, const int party, const int t, const u6
 }
 
 template <int W, int TP, bool RING64>
-__global__ void __launch_bounds__(2 * TP, HB_PAIR_MINB) k_relu_pair(const PairArgs A) {
+__global__ void __launch_bounds__(2 * TP, pair_minb<W>()) k_relu_pair(const PairArgs A) {
   constexpr int GS = Geo<W>::GS;
   extern __shared__ u64 wire[];  // [buf 2][party 2][SEGW][TP]
   const int party = threadIdx.x >= TP ? 1 : 0;
