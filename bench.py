@@ -417,9 +417,10 @@ def run_single(args):
                      "alg_bytes_per_elem_per_party": alg_bpe, "survey_H_bytes_per_elem_per_party": bpe["survey_H"],
                      "frac_vs_survey_H": (2 * n * bpe["survey_H"] / (launch_ms / 1e3) / 1e9) / peak,
                      "kernel": "hb::" + kernel, "traffic_source": traffic_src, "launch_ms": launch_ms,
-                     "peak_note": "peak = the driver's copy benchmark (1 read : 1 write); this kernel reads 77 of "
-                                  "its 85 B per element and party, and read-only streaming reaches ~6.83 TB/s on "
-                                  "these boxes (profiles/hbm_stream_rates_r02.json), so frac can exceed 1"},
+                     "peak_note": "peak = the driver's copy benchmark (1 read : 1 write); the ReLU kernels mostly "
+                                  "read (x and the triples; w = 8: 77 of 85 B per element and party) and read-only "
+                                  "streaming reaches ~6.83 TB/s on these boxes (profiles/hbm_stream_rates_r02.json), "
+                                  "so frac can exceed 1"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
         "resnet18": resnet, "desk_cnn": desk,
     }
